@@ -1,0 +1,401 @@
+// capi.cu -- the extern "C" boundary (include/knn_b200.h).
+//
+// Validation order and exception text follow the reference exactly
+// (paths relative to /root/reference/proj):
+//   PointSet construction ........ include/knn/point_set.hpp:18-31
+//   Metric::mahalanobis .......... src/metric.cpp:20-61
+//   bf_knn ....................... src/bruteforce.cpp:44-56
+//   Metric::check_compatible ..... include/knn/metric.hpp:90-96
+// Invalid arguments map to KNN_B200_EINVAL with that text in
+// knn_b200_last_error(); the C++ mirror rethrows them as std::invalid_argument.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/knn_b200.h"
+#include "common.cuh"
+#include "engine.cuh"
+#include "exact_kernel.cuh"
+
+namespace knnb200 {
+
+namespace {
+thread_local std::string g_last_error;
+thread_local uint64_t g_launches = 0;
+
+knn_b200_status fail(knn_b200_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+template <typename F>
+knn_b200_status guarded(F&& body) {
+    try {
+        g_last_error.clear();
+        body();
+        return KNN_B200_OK;
+    } catch (const InvalidArgument& e) {
+        return fail(KNN_B200_EINVAL, e.what());
+    } catch (const OutOfMemory& e) {
+        return fail(KNN_B200_ENOMEM, e.what());
+    } catch (const CudaError& e) {
+        return fail(KNN_B200_ECUDA, e.what());
+    } catch (const std::bad_alloc& e) {
+        return fail(KNN_B200_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(KNN_B200_EINTERNAL, e.what());
+    }
+}
+
+const knn_b200_options& opts_or_default(const knn_b200_options* opt, knn_b200_options& tmp) {
+    if (opt) return *opt;
+    knn_b200_options_init(&tmp);
+    return tmp;
+}
+
+void check_point_set(const float* data, int64_t n, int64_t d, bool check_values) {
+    if (n <= 0) throw InvalidArgument("PointSet: point count must be >= 1");
+    if (d <= 0) throw InvalidArgument("PointSet: dimension must be >= 1");
+    if (!data) throw InvalidArgument("PointSet: null data pointer");
+    if (!check_values) return;
+    const int64_t total = n * d;
+    for (int64_t i = 0; i < total; ++i) {
+        if (!std::isfinite(data[i])) {
+            throw InvalidArgument("PointSet: non-finite coordinate at point " +
+                                  std::to_string(i / d) + ", dimension " +
+                                  std::to_string(i % d));
+        }
+    }
+}
+
+// Metric::mahalanobis (metric.cpp:20-61): validate, Cholesky M = L L^T.
+std::vector<double> cholesky_or_throw(const double* M, int64_t d) {
+    if (d <= 0) throw InvalidArgument("Metric: Mahalanobis dimension must be >= 1");
+    if (!M) throw InvalidArgument("Metric: Mahalanobis matrix has 0 entries, expected " +
+                                  std::to_string(d * d));
+    for (int64_t i = 0; i < d; ++i)
+        for (int64_t j = i + 1; j < d; ++j) {
+            const double a = M[i * d + j], b = M[j * d + i];
+            if (std::abs(a - b) > 1e-12 * std::max(std::abs(a), std::abs(b)))
+                throw InvalidArgument("Metric: Mahalanobis matrix is not symmetric at (" +
+                                      std::to_string(i) + "," + std::to_string(j) + ")");
+        }
+    std::vector<double> L(static_cast<size_t>(d * d), 0.0);
+    for (int64_t i = 0; i < d; ++i)
+        for (int64_t j = 0; j <= i; ++j) {
+            double s = M[i * d + j];
+            for (int64_t c = 0; c < j; ++c) s -= L[i * d + c] * L[j * d + c];
+            if (i == j) {
+                if (!(s > 0.0))
+                    throw InvalidArgument(
+                        "Metric: Mahalanobis matrix is not positive definite (pivot " +
+                        std::to_string(i) + ")");
+                L[i * d + i] = std::sqrt(s);
+            } else {
+                L[i * d + j] = s / L[j * d + j];
+            }
+        }
+    return L;
+}
+
+// y = L^T x in double on widened inputs (metric.cpp:63-82), narrowed to FP32
+// for the Euclidean kernel the metric collapses to (metric.hpp:81-83).
+std::vector<float> whiten(const std::vector<double>& L, const float* x, int64_t n, int64_t d) {
+    std::vector<float> out(static_cast<size_t>(n * d));
+    std::vector<double> row(static_cast<size_t>(d));
+    for (int64_t p = 0; p < n; ++p) {
+        for (int64_t c = 0; c < d; ++c) row[c] = x[p * d + c];
+        for (int64_t r = 0; r < d; ++r) {
+            double acc = 0.0;
+            for (int64_t c = r; c < d; ++c) acc += L[c * d + r] * row[c];
+            out[p * d + r] = static_cast<float>(acc);
+        }
+    }
+    return out;
+}
+
+// bruteforce.cpp:44-56 in order, then Metric::check_compatible.
+void check_search(int64_t dq, int64_t dr, int64_t m, int64_t k, const knn_b200_options& o,
+                  int metric) {
+    if (dq != dr)
+        throw InvalidArgument("bf_knn: dimension mismatch, queries have " + std::to_string(dq) +
+                              ", references have " + std::to_string(dr));
+    if (k <= 0) throw InvalidArgument("bf_knn: k must be >= 1");
+    if (k > m)
+        throw InvalidArgument("bf_knn: k = " + std::to_string(k) + " exceeds reference count " +
+                              std::to_string(m));
+    if (o.chunk_size == 0) throw InvalidArgument("bf_knn: chunk_size must be >= 1");
+    if (metric < 0 || metric > 3) throw InvalidArgument("bf_knn: unknown metric");
+    if (metric == kMahalanobis && o.mahalanobis_dim != dq)
+        throw InvalidArgument("Metric: Mahalanobis matrix is " + std::to_string(o.mahalanobis_dim) +
+                              "x" + std::to_string(o.mahalanobis_dim) +
+                              " but points have dimension " + std::to_string(dq));
+    if (k > 0x7ffffffe || m > 0x7ffffffe)
+        throw InvalidArgument("bf_knn: k and m must be < 2^31 per device search");
+}
+
+}  // namespace
+
+void note_launch(int count) { g_launches += static_cast<uint64_t>(count); }
+
+}  // namespace knnb200
+
+using namespace knnb200;
+
+struct knn_b200_index {
+    int device = 0;
+    const float* dR = nullptr;
+    bool owned = false;
+    int64_t m = 0;
+    int d = 0;
+    int64_t base = 0;
+    std::mutex mu;
+    ~knn_b200_index() {
+        if (owned && dR) cudaFree(const_cast<float*>(dR));
+    }
+};
+
+extern "C" {
+
+void knn_b200_options_init(knn_b200_options* opt) {
+    if (!opt) return;
+    std::memset(opt, 0, sizeof(*opt));
+    opt->struct_size = sizeof(*opt);
+    opt->device = -1;
+    opt->path = KNN_B200_PATH_AUTO;
+    opt->chunk_size = 1024;  // BfConfig default (bruteforce.hpp:15)
+}
+
+const char* knn_b200_last_error(void) { return g_last_error.c_str(); }
+
+const char* knn_b200_version(void) { return "knn_b200 0.1 (sm_100a)"; }
+
+uint64_t knn_b200_launch_count(void) { return g_launches; }
+void knn_b200_reset_launch_count(void) { g_launches = 0; }
+
+knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
+                                const float* references, int64_t m, int32_t dr, int32_t k,
+                                int32_t metric, const knn_b200_options* opt, float* out_dist,
+                                int64_t* out_idx, uint64_t* distance_evals) {
+    return guarded([&] {
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        std::vector<double> chol;
+        if (metric == kMahalanobis) chol = cholesky_or_throw(o.mahalanobis, o.mahalanobis_dim);
+        check_point_set(queries, n, dq, true);
+        check_point_set(references, m, dr, true);
+        check_search(dq, dr, m, k, o, metric);
+        if (!out_dist || !out_idx) throw InvalidArgument("bf_knn: null output pointer");
+
+        std::vector<float> wq, wr;
+        const float* q = queries;
+        const float* r = references;
+        int kernel_metric = metric;
+        if (metric == kMahalanobis) {
+            wq = whiten(chol, queries, n, dq);
+            wr = whiten(chol, references, m, dr);
+            q = wq.data();
+            r = wr.data();
+            kernel_metric = kL2;
+        }
+
+        DeviceContext& ctx = context_for(o.device);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        cudaStream_t s = ctx.stream;
+        Sizer sz;
+        sz.take<float>(static_cast<size_t>(n) * dq);
+        sz.take<float>(static_cast<size_t>(m) * dr);
+        sz.take<float>(static_cast<size_t>(n) * k);
+        sz.take<int64_t>(static_cast<size_t>(n) * k);
+        ctx.io.reserve(sz.used + 256);
+        Carver cv{static_cast<char*>(ctx.io.base())};
+        float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
+        float* dR = cv.take<float>(static_cast<size_t>(m) * dr);
+        float* dO = cv.take<float>(static_cast<size_t>(n) * k);
+        int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, q, sizeof(float) * n * dq, cudaMemcpyHostToDevice, s));
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * dr, cudaMemcpyHostToDevice, s));
+        search_device(ctx, s, dQ, n, dR, m, dq, k, kernel_metric, o.path, o.raw_keys, 0, dO, dI);
+        KNN_CUDA_CHECK(
+            cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
+        KNN_CUDA_CHECK(
+            cudaMemcpyAsync(out_idx, dI, sizeof(int64_t) * n * k, cudaMemcpyDeviceToHost, s));
+        KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (distance_evals)
+            *distance_evals = o.count_distance_evals ? static_cast<uint64_t>(n) * m : 0;
+    });
+}
+
+knn_b200_status knn_b200_search_device(const float* d_queries, int64_t n,
+                                       const float* d_references, int64_t m, int32_t d,
+                                       int32_t k, int32_t metric, const knn_b200_options* opt,
+                                       float* d_out_dist, int64_t* d_out_idx) {
+    return guarded([&] {
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        if (metric == kMahalanobis)
+            throw InvalidArgument("knn_b200_search_device: whiten inputs for Mahalanobis");
+        check_point_set(d_queries, n, d, false);
+        check_point_set(d_references, m, d, false);
+        check_search(d, d, m, k, o, metric);
+        if (!d_out_dist || !d_out_idx) throw InvalidArgument("bf_knn: null output pointer");
+        DeviceContext& ctx = context_for(o.device);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        search_device(ctx, s, d_queries, n, d_references, m, d, k, metric, o.path, o.raw_keys, 0,
+                      d_out_dist, d_out_idx);
+        if (!o.stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+knn_b200_status knn_b200_index_create(const float* references, int64_t m, int32_t d,
+                                      int64_t index_base, const knn_b200_options* opt,
+                                      knn_b200_index** out) {
+    return guarded([&] {
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        if (!out) throw InvalidArgument("knn_b200_index_create: null out");
+        check_point_set(references, m, d, true);
+        DeviceContext& ctx = context_for(o.device);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        auto* h = new knn_b200_index();
+        h->device = ctx.device;
+        h->m = m;
+        h->d = d;
+        h->base = index_base;
+        float* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, sizeof(float) * m * d);
+        if (e != cudaSuccess) {
+            delete h;
+            KNN_CUDA_CHECK(e);
+        }
+        h->dR = p;
+        h->owned = true;
+        e = cudaMemcpy(p, references, sizeof(float) * m * d, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            delete h;
+            KNN_CUDA_CHECK(e);
+        }
+        *out = h;
+    });
+}
+
+knn_b200_status knn_b200_index_create_device(const float* d_references, int64_t m, int32_t d,
+                                             int64_t index_base, const knn_b200_options* opt,
+                                             knn_b200_index** out) {
+    return guarded([&] {
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        if (!out) throw InvalidArgument("knn_b200_index_create: null out");
+        check_point_set(d_references, m, d, false);
+        DeviceContext& ctx = context_for(o.device);
+        auto* h = new knn_b200_index();
+        h->device = ctx.device;
+        h->dR = d_references;
+        h->owned = false;
+        h->m = m;
+        h->d = d;
+        h->base = index_base;
+        *out = h;
+    });
+}
+
+knn_b200_status knn_b200_index_search(knn_b200_index* index, const float* queries, int64_t n,
+                                      int32_t k, int32_t metric, const knn_b200_options* opt,
+                                      float* out_dist, int64_t* out_idx) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("knn_b200_index_search: null index");
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        if (metric == kMahalanobis)
+            throw InvalidArgument("knn_b200_index_search: whiten inputs for Mahalanobis");
+        check_point_set(queries, n, index->d, true);
+        check_search(index->d, index->d, index->m, k, o, metric);
+        DeviceContext& ctx = context_for(index->device);
+        std::lock_guard<std::mutex> hl(index->mu);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        Sizer sz;
+        sz.take<float>(static_cast<size_t>(n) * index->d);
+        sz.take<float>(static_cast<size_t>(n) * k);
+        sz.take<int64_t>(static_cast<size_t>(n) * k);
+        ctx.io.reserve(sz.used + 256);
+        Carver cv{static_cast<char*>(ctx.io.base())};
+        float* dQ = cv.take<float>(static_cast<size_t>(n) * index->d);
+        float* dO = cv.take<float>(static_cast<size_t>(n) * k);
+        int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, queries, sizeof(float) * n * index->d,
+                                       cudaMemcpyHostToDevice, s));
+        search_device(ctx, s, dQ, n, index->dR, index->m, index->d, k, metric, o.path,
+                      o.raw_keys, index->base, dO, dI);
+        KNN_CUDA_CHECK(
+            cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
+        KNN_CUDA_CHECK(
+            cudaMemcpyAsync(out_idx, dI, sizeof(int64_t) * n * k, cudaMemcpyDeviceToHost, s));
+        KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+knn_b200_status knn_b200_index_search_device(knn_b200_index* index, const float* d_queries,
+                                             int64_t n, int32_t k, int32_t metric,
+                                             const knn_b200_options* opt, float* d_out_dist,
+                                             int64_t* d_out_idx) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("knn_b200_index_search: null index");
+        knn_b200_options tmp;
+        const knn_b200_options& o = opts_or_default(opt, tmp);
+        if (metric == kMahalanobis)
+            throw InvalidArgument("knn_b200_index_search: whiten inputs for Mahalanobis");
+        check_point_set(d_queries, n, index->d, false);
+        check_search(index->d, index->d, index->m, k, o, metric);
+        DeviceContext& ctx = context_for(index->device);
+        std::lock_guard<std::mutex> hl(index->mu);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        search_device(ctx, s, d_queries, n, index->dR, index->m, index->d, k, metric, o.path,
+                      o.raw_keys, index->base, d_out_dist, d_out_idx);
+        if (!o.stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+void knn_b200_index_destroy(knn_b200_index* index) { delete index; }
+
+knn_b200_status knn_b200_merge_device(const float* d_part_keys, const int64_t* d_part_idx,
+                                      int32_t parts, int64_t n, int32_t k, int32_t metric,
+                                      void* stream, float* d_out_dist, int64_t* d_out_idx) {
+    return guarded([&] {
+        if (parts <= 0 || n <= 0 || k <= 0)
+            throw InvalidArgument("knn_b200_merge_device: parts, n and k must be >= 1");
+        DeviceContext& ctx = context_for(-1);
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx.stream;
+        MergeArgs mg{};
+        mg.part_key = d_part_keys;
+        mg.part_idx = d_part_idx;
+        mg.parts = parts;
+        mg.n = n;
+        mg.k = k;
+        mg.metric = metric == kMahalanobis ? kL2 : metric;
+        mg.finalize = 1;
+        mg.out_key = d_out_dist;
+        mg.out_idx = d_out_idx;
+        if (k > 1024) {
+            Sizer sz;
+            sz.take<float>(static_cast<size_t>(n) * k);
+            sz.take<int64_t>(static_cast<size_t>(n) * k);
+            ctx.arena.reserve(sz.used + 256);
+            Carver cv{static_cast<char*>(ctx.arena.base())};
+            mg.glist_key = cv.take<float>(static_cast<size_t>(n) * k);
+            mg.glist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
+        }
+        launch_merge(mg, s);
+        if (!stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// engine.cu -- search orchestration on one device.
+//
+// The reference's bf_knn (src/bruteforce.cpp:42-100) processes queries in
+// chunks of chunk_size rows with an OpenMP fork/join per chunk and a
+// chunk x m double scratch.  Here one search is a short fixed sequence of
+// kernel launches on one stream with all scratch carved from a grow-only
+// per-device arena:
+//   exact path   exact_knn_kernel (fused keys + top-k per reference split)
+//                [+ merge_kernel when the reference axis was split]
+//   tensor path  see tensor_kernel.cu (prep -> tcgen05 candidates ->
+//                exact re-rank -> exact fallback for uncertified queries)
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <memory>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "exact_kernel.cuh"
+#include "tensor_path.cuh"
+
+namespace knnb200 {
+
+DeviceArena::~DeviceArena() {
+    if (base_) cudaFree(base_);
+}
+
+void DeviceArena::reserve(size_t bytes) {
+    if (bytes <= cap_) return;
+    if (base_) {
+        KNN_CUDA_CHECK(cudaDeviceSynchronize());
+        KNN_CUDA_CHECK(cudaFree(base_));
+        base_ = nullptr;
+        cap_ = 0;
+    }
+    const size_t want = std::max(bytes, cap_ + cap_ / 2);
+    KNN_CUDA_CHECK(cudaMalloc(&base_, want));
+    cap_ = want;
+}
+
+DeviceContext& context_for(int device) {
+    static std::mutex registry_mu;
+    static std::map<int, std::unique_ptr<DeviceContext>> registry;
+    if (device < 0) KNN_CUDA_CHECK(cudaGetDevice(&device));
+    std::lock_guard<std::mutex> lock(registry_mu);
+    auto& slot = registry[device];
+    if (!slot) {
+        slot = std::make_unique<DeviceContext>();
+        slot->device = device;
+        KNN_CUDA_CHECK(cudaSetDevice(device));
+        KNN_CUDA_CHECK(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+    }
+    return *slot;
+}
+
+SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path) {
+    SearchPlan p{};
+    p.path = 1;
+    if (path != 1 && metric == kL2 && tensor_path_supported(n, m, d, k)) p.path = 2;
+    if (path == 2 && p.path != 2 && metric == kL2 && !tensor_path_supported(n, m, d, k))
+        p.path = 1;  // TENSOR requested for an unsupported shape: exact gives identical results
+    // exact path: split the reference axis until there are >= ~4 waves of
+    // CTAs (3 resident per SM); every split keeps >= max(k, 1024) references
+    const int64_t ctas_x = (n + exact_queries_per_cta() - 1) / exact_queries_per_cta();
+    const int64_t want = (4LL * kSmCount * 3 + ctas_x - 1) / ctas_x;
+    const int64_t max_splits = std::max<int64_t>(1, m / std::max<int64_t>(k, 1024));
+    p.splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, max_splits)));
+    p.splits = std::min(p.splits, 64);
+    return p;
+}
+
+static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                      const float* dR, int64_t m, int d, int k, int metric, int splits,
+                      int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx) {
+    const bool big_k = static_cast<size_t>(k) > exact_smem_list_limit_k();
+    ExactArgs a{};
+    a.Q = dQ;
+    a.R = dR;
+    a.n = n;
+    a.m = m;
+    a.d = d;
+    a.k = k;
+    a.splits = splits;
+    a.split_len = (m + splits - 1) / splits;
+    a.index_base = index_base;
+
+    Sizer sz;
+    if (splits > 1) {
+        sz.take<float>(static_cast<size_t>(splits) * n * k);
+        sz.take<int64_t>(static_cast<size_t>(splits) * n * k);
+    }
+    const size_t lists = exact_cta_count(n, splits) * exact_queries_per_cta() * k;
+    if (big_k) {
+        sz.take<float>(lists);
+        sz.take<int32_t>(lists);
+    }
+    if (splits > 1 && static_cast<size_t>(k) > 1024) {
+        sz.take<float>(static_cast<size_t>(n) * k);
+        sz.take<int64_t>(static_cast<size_t>(n) * k);
+    }
+    ctx.arena.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.arena.base())};
+    float* part_key = d_out;
+    int64_t* part_idx = d_idx;
+    if (splits > 1) {
+        part_key = cv.take<float>(static_cast<size_t>(splits) * n * k);
+        part_idx = cv.take<int64_t>(static_cast<size_t>(splits) * n * k);
+    }
+    if (big_k) {
+        a.glist_key = cv.take<float>(lists);
+        a.glist_idx = cv.take<int32_t>(lists);
+    }
+    a.out_key = part_key;
+    a.out_idx = part_idx;
+    a.finalize = (splits == 1 && !raw_keys) ? 1 : 0;
+    launch_exact(metric, a, stream);
+
+    if (splits > 1) {
+        MergeArgs mg{};
+        mg.part_key = part_key;
+        mg.part_idx = part_idx;
+        mg.parts = splits;
+        mg.n = n;
+        mg.k = k;
+        mg.metric = metric;
+        mg.finalize = raw_keys ? 0 : 1;
+        mg.out_key = d_out;
+        mg.out_idx = d_idx;
+        if (static_cast<size_t>(k) > 1024) {
+            mg.glist_key = cv.take<float>(static_cast<size_t>(n) * k);
+            mg.glist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
+        }
+        launch_merge(mg, stream);
+    }
+}
+
+void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                   const float* dR, int64_t m, int d, int k, int metric, int path,
+                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx) {
+    const SearchPlan plan = plan_search(n, m, d, k, metric, path);
+    if (plan.path == 2) {
+        run_tensor_path(ctx, stream, dQ, n, dR, m, d, k, raw_keys, index_base, d_out, d_idx);
+        return;
+    }
+    run_exact(ctx, stream, dQ, n, dR, m, d, k, metric, plan.splits, raw_keys, index_base, d_out,
+              d_idx);
+}
+
+// exposed for the tensor path's fallback on uncertified queries
+void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
+                      float* d_out, int64_t* d_idx) {
+    const SearchPlan plan = plan_search(n, m, d, k, kL2, 1);
+    run_exact(ctx, stream, dQ, n, dR, m, d, k, kL2, plan.splits, raw_keys, index_base, d_out,
+              d_idx);
+}
+
+}  // namespace knnb200

@@ -1,0 +1,70 @@
+// engine.cuh -- host-side engine: device contexts, workspaces, search plans.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <vector>
+
+namespace knnb200 {
+
+// Grow-only device scratch arena (one per context).  Carves aligned slices
+// out of one allocation so a search does a single cudaMalloc at most.
+class DeviceArena {
+public:
+    ~DeviceArena();
+    void reserve(size_t bytes);
+    void* base() const { return base_; }
+
+private:
+    void* base_ = nullptr;
+    size_t cap_ = 0;
+};
+
+struct Carver {
+    char* p;
+    size_t used = 0;
+    template <typename T>
+    T* take(size_t count) {
+        used = (used + 255) & ~static_cast<size_t>(255);
+        T* out = reinterpret_cast<T*>(p + used);
+        used += count * sizeof(T);
+        return out;
+    }
+};
+
+// Bytes a Carver needs for the given take() sizes (same 256 B alignment).
+struct Sizer {
+    size_t used = 0;
+    template <typename T>
+    void take(size_t count) {
+        used = (used + 255) & ~static_cast<size_t>(255);
+        used += count * sizeof(T);
+    }
+};
+
+struct DeviceContext {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DeviceArena arena;       // per-search scratch
+    DeviceArena io;          // host-API staging of inputs / outputs
+    std::mutex mu;           // one search at a time per context
+};
+
+DeviceContext& context_for(int device);  // device < 0: current device
+
+struct SearchPlan {
+    int path;       // 1 exact, 2 tensor
+    int splits;     // reference-axis splits for the exact path
+};
+
+// Core device search.  All pointers are device pointers.  Output: finalized
+// distances (or raw keys when raw_keys) and global indices (index_base + j).
+void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                   const float* dR, int64_t m, int d, int k, int metric, int path,
+                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx);
+
+SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path);
+
+}  // namespace knnb200

@@ -1,0 +1,124 @@
+// warp_list.cuh -- warp-cooperative sorted top-k list.
+//
+// Replaces the reference's per-row select_k_smallest (src/topk.cpp:17-33:
+// nth_element + sort over a materialised m-long row) with a streaming
+// structure: a list of the k best (key, index) pairs seen so far, kept sorted
+// ascending under the (key, index) order, stored in shared (or global) memory
+// and updated by one warp.  Candidates are filtered against the list's k-th
+// entry (the running threshold) before any insertion, so after the first few
+// tiles almost every candidate is rejected with one compare.
+//
+// Layout: entry i of a list lives at key[i], idx[i] (i < k).  Unfilled slots
+// hold the sentinel (+inf, INT64_MAX), so the threshold is always key[k-1].
+#pragma once
+
+#include "common.cuh"
+
+namespace knnb200 {
+
+template <typename IdxT>
+__device__ __forceinline__ IdxT sentinel_of() {
+    return sizeof(IdxT) == 8 ? static_cast<IdxT>(kSentinelIdx) : static_cast<IdxT>(0x7fffffff);
+}
+
+template <typename IdxT>
+struct WarpList {
+    float* key;  // k entries
+    IdxT* idx;   // k entries
+    int k;
+
+    __device__ __forceinline__ void init(int lane) {
+        for (int i = lane; i < k; i += 32) {
+            key[i] = kInf;
+            idx[i] = sentinel_of<IdxT>();
+        }
+    }
+
+    // Threshold: the current k-th best (all lanes get the same value).
+    __device__ __forceinline__ void threshold(float& tk, int64_t& ti) const {
+        tk = key[k - 1];
+        ti = static_cast<int64_t>(idx[k - 1]);
+    }
+
+    // Insert one candidate known to beat the threshold.  All 32 lanes call it
+    // with the same (x, jx).  Cost ~ (k/32) x (2 loads + compare + ballot).
+    __device__ void insert(float x, int64_t jx, int lane) {
+        const int chunks = (k + 31) >> 5;
+        int pos = 0;
+        for (int r = 0; r < chunks; ++r) {
+            const int i = lane + (r << 5);
+            bool lt = false;
+            if (i < k) lt = pair_less(key[i], static_cast<int64_t>(idx[i]), x, jx);
+            pos += __popc(__ballot_sync(0xffffffffu, lt));
+        }
+        // shift [pos, k-1) up by one, high chunks first
+        for (int r = chunks - 1; r >= 0; --r) {
+            const int i = lane + (r << 5);
+            if ((r << 5) + 31 < pos) break;  // whole chunk below pos: untouched (warp-uniform)
+            float nk = 0.f;
+            IdxT ni = 0;
+            const bool mv = i < k && i > pos;
+            if (mv) {
+                nk = key[i - 1];
+                ni = idx[i - 1];
+            }
+            __syncwarp();
+            if (mv) {
+                key[i] = nk;
+                idx[i] = ni;
+            } else if (i == pos) {
+                key[i] = x;
+                idx[i] = static_cast<IdxT>(jx);
+            }
+            __syncwarp();
+        }
+    }
+
+    // Offer up to 32 x P candidates held P per lane (keys/indices in small
+    // register arrays, invalid ones = +inf / sentinel).  Inserts every one that
+    // beats the running threshold, in any order (the list is order-free).
+    template <int P>
+    __device__ void offer(const float (&ck)[P], const int64_t (&ci)[P], int lane) {
+        float tk;
+        int64_t ti;
+        threshold(tk, ti);
+        unsigned pending = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (pair_less(ck[p], ci[p], tk, ti)) pending |= 1u << p;
+        while (__any_sync(0xffffffffu, pending != 0)) {
+            // each lane exposes its lowest pending candidate
+            float myk = kInf;
+            int64_t myi = kSentinelIdx;
+            int myp = -1;
+            if (pending) {
+                myp = __ffs(pending) - 1;
+#pragma unroll
+                for (int p = 0; p < P; ++p)
+                    if (p == myp) {
+                        myk = ck[p];
+                        myi = ci[p];
+                    }
+            }
+            unsigned who = __ballot_sync(0xffffffffu, pending != 0);
+            while (who) {
+                const int src = __ffs(who) - 1;
+                who &= who - 1;
+                const float x = __shfl_sync(0xffffffffu, myk, src);
+                const int64_t jx = __shfl_sync(0xffffffffu, myi, src);
+                if (pair_less(x, jx, tk, ti)) {
+                    insert(x, jx, lane);
+                    threshold(tk, ti);
+                }
+            }
+            if (myp >= 0) pending &= ~(1u << myp);
+            // drop what the tightened threshold now rejects
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                if ((pending >> p) & 1u)
+                    if (!pair_less(ck[p], ci[p], tk, ti)) pending &= ~(1u << p);
+        }
+    }
+};
+
+}  // namespace knnb200

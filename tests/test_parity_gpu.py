@@ -1,0 +1,242 @@
+"""GPU parity tests: the CUDA engine (through the C ABI) against the oracle and
+the reference's golden outputs, with the north-star tolerance comparator
+(distances within 1e-5 relative; index differences only at near-ties).
+
+Mirrors the reference's own hot-path tests (paths relative to
+/root/reference/proj/tests): test_bruteforce.cpp (hand-checked KATs, contract
+errors, random instances vs the serial oracle, determinism, evaluation count)
+and acceptance.cpp C1 / C3 / C9.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import CHEBYSHEV, EUCLIDEAN, MAHALANOBIS, MANHATTAN, compare
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ("exact", "tensor", "auto")
+
+
+def cfg(knn, path):
+    p = {"exact": knn.PATH_EXACT, "tensor": knn.PATH_TENSOR, "auto": knn.PATH_AUTO}[path]
+    return knn.BfConfig(path=p, device=0)
+
+
+def metric_of(knn, kind, mahal=None):
+    if kind == MAHALANOBIS:
+        d = int(round(len(mahal) ** 0.5))
+        return knn.Metric.mahalanobis(d, mahal)
+    return knn.Metric(kind)
+
+
+def check_invariants(table, m):
+    """test_bruteforce.cpp:22-39: range, distinct, ascending, ties by index."""
+    idx, dist = table.index, table.distance
+    assert (idx >= 0).all() and (idx < m).all()
+    for i in range(idx.shape[0]):
+        assert len(set(idx[i].tolist())) == idx.shape[1]
+        dd = dist[i]
+        assert (np.diff(dd) >= 0).all()
+        same = np.nonzero(np.diff(dd) == 0)[0]
+        assert (idx[i][same + 1] > idx[i][same]).all()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_golden_reference_outputs(knn, golden, oracle, path):
+    """Every golden case (reference's own outputs, tests/golden/) within tolerance."""
+    for name, c in golden.items():
+        kind = int(c["metric"])
+        mahal = c["mahal"] if kind == MAHALANOBIS else None
+        t = knn.bf_knn(c["Q"], c["R"], int(c["k"]), metric_of(knn, kind, mahal),
+                       config=cfg(knn, path))
+        rep = compare(t.index, t.distance, c["idx"], c["dist"], c["Q"], c["R"], kind,
+                      oracle=oracle, mahal=mahal, atol=1e-6)
+        assert rep.ok, f"{name}: {rep}"
+        check_invariants(t, c["R"].shape[0])
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_collinear_and_full_sort(knn, path):
+    # test_bruteforce.cpp:77-90
+    R = np.array([[0, 0], [1, 0], [2, 0]], np.float32)
+    Q = np.array([[0.1, 0]], np.float32)
+    t = knn.bf_knn(Q, R, 2, config=cfg(knn, path))
+    assert t.index[0].tolist() == [0, 1]
+    assert t.distance[0, 0] == pytest.approx(0.1, rel=1e-6)
+    assert t.distance[0, 1] == pytest.approx(0.9, rel=1e-6)
+    full = knn.bf_knn(Q, R, 3, config=cfg(knn, path))
+    assert full.index[0, 2] == 2
+    check_invariants(full, 3)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_all_duplicates_resolve_to_lowest_indices(knn, path):
+    # test_kdtree.cpp:65-75
+    P = np.full((64, 3), 1.5, np.float32)
+    t = knn.bf_knn(np.full((1, 3), 1.5, np.float32), P, 5, config=cfg(knn, path))
+    assert t.index[0].tolist() == [0, 1, 2, 3, 4]
+    assert (t.distance == 0).all()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_self_join_has_exact_zero_self_match(knn, oracle, path):
+    # entropy.cpp:48-57 relies on the self match appearing at distance 0 in k+1
+    P = oracle.uniform_f32(700, 24, 77)
+    t = knn.bf_knn(P, P, 5, config=cfg(knn, path))
+    assert (t.distance[:, 0] == 0).all()
+    assert (t.index[:, 0] == np.arange(700)).all()
+
+
+@pytest.mark.parametrize("metric", [EUCLIDEAN, MANHATTAN, CHEBYSHEV, MAHALANOBIS])
+def test_random_instances_vs_oracle(knn, oracle, metric):
+    """acceptance.cpp:58-84 style (C1), tolerance instead of bitwise."""
+    rng = np.random.default_rng(1001 + metric)
+    spd = np.array([2.0, 0.4, 0.0, 0.4, 1.5, -0.2, 0.0, -0.2, 1.0])
+    for trial in range(25):
+        n, m = int(rng.integers(1, 300)), int(rng.integers(1, 700))
+        d = 3 if metric == MAHALANOBIS else int(rng.integers(1, 70))
+        k = int(rng.integers(1, min(m, 300) + 1))
+        Q = (rng.random((n, d)) * 10 - 5).astype(np.float32)
+        R = (rng.random((m, d)) * 10 - 5).astype(np.float32)
+        mahal = spd if metric == MAHALANOBIS else None
+        ri, rd = oracle.knn(Q, R, k, metric, mahal)
+        for path in PATHS:
+            t = knn.bf_knn(Q, R, k, metric_of(knn, metric, mahal), config=cfg(knn, path))
+            rep = compare(t.index, t.distance, ri, rd, Q, R, metric, oracle=oracle, mahal=mahal,
+                          atol=1e-6)
+            assert rep.ok, f"trial {trial} n={n} m={m} d={d} k={k} path={path}: {rep}"
+
+
+@pytest.mark.parametrize("k", [1, 20, 100, 256, 1024])
+def test_k_sweep_subsample(knn, oracle, k):
+    """Config D shape (m=38400, d=64) on a 192-query subsample, k up to 1024."""
+    m, d = 38400, 64
+    R = oracle.uniform_f32(m, d, oracle.derive_seed(42, m, d, 0))
+    Q = oracle.uniform_f32(192, d, oracle.derive_seed(42, m, d, 1))
+    ri, rd = oracle.knn(Q, R, k)
+    for path in PATHS:
+        t = knn.bf_knn(Q, R, k, config=cfg(knn, path))
+        rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+        assert rep.ok, f"k={k} path={path}: {rep}"
+
+
+@pytest.mark.parametrize("d", [8, 16, 32, 64, 80, 96, 128])
+def test_d_sweep_subsample(knn, oracle, d):
+    """Config C shape (m=19200, k=20) on a 256-query subsample."""
+    m = 19200
+    R = oracle.uniform_f32(m, d, oracle.derive_seed(42, m, d, 0))
+    Q = oracle.uniform_f32(256, d, oracle.derive_seed(42, m, d, 1))
+    ri, rd = oracle.knn(Q, R, 20)
+    for path in PATHS:
+        t = knn.bf_knn(Q, R, 20, config=cfg(knn, path))
+        rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+        assert rep.ok, f"d={d} path={path}: {rep}"
+
+
+def test_config_a_full(knn, oracle):
+    """BASELINE configs[0]: m=n=4800, d=32, k=20, every query."""
+    R = oracle.uniform_f32(4800, 32, oracle.derive_seed(42, 4800, 32, 0))
+    Q = oracle.uniform_f32(4800, 32, oracle.derive_seed(42, 4800, 32, 1))
+    ri, rd = oracle.knn(Q, R, 20)
+    for path in PATHS:
+        t = knn.bf_knn(Q, R, 20, config=cfg(knn, path))
+        rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+        assert rep.ok, f"path={path}: {rep}"
+
+
+def test_config_b_subsample(knn, oracle):
+    """BASELINE configs[1] (headline): m=n=38400, d=96, k=20; full search on the
+    GPU, 512 queries checked against the oracle, the rest via invariants."""
+    m = n = 38400
+    d = 96
+    R = oracle.uniform_f32(m, d, oracle.derive_seed(42, m, d, 0))
+    Q = oracle.uniform_f32(n, d, oracle.derive_seed(42, n, d, 1))
+    t = knn.bf_knn(Q, R, 20, config=cfg(knn, "auto"))
+    sel = np.linspace(0, n - 1, 512).astype(int)
+    ri, rd = oracle.knn(Q[sel], R, 20)
+    rep = compare(t.index[sel], t.distance[sel], ri, rd, Q[sel], R, oracle=oracle)
+    assert rep.ok, str(rep)
+    check_invariants(t, m)
+
+
+def test_paths_are_bitwise_identical(knn, oracle):
+    """C3 analogue: exact / tensor / auto give bitwise-equal tables."""
+    R = oracle.uniform_f32(9000, 40, 11)
+    Q = oracle.uniform_f32(1000, 40, 12)
+    tabs = [knn.bf_knn(Q, R, 17, config=cfg(knn, p)) for p in PATHS]
+    for t in tabs[1:]:
+        assert (t.index == tabs[0].index).all()
+        assert (t.distance == tabs[0].distance).all()
+
+
+def test_chunk_and_workers_do_not_change_results(knn, oracle):
+    # test_bruteforce.cpp:124-136
+    R = oracle.uniform_f32(53, 6, 102)
+    Q = oracle.uniform_f32(37, 6, 101)
+    base = knn.bf_knn(Q, R, 7)
+    for workers in (1, 2, 8):
+        for chunk in (1, 7, 37):
+            t = knn.bf_knn(Q, R, 7, config=knn.BfConfig(chunk_size=chunk, worker_count=workers))
+            assert (t.index == base.index).all() and (t.distance == base.distance).all()
+
+
+def test_distance_evals_is_n_times_m(knn, oracle):
+    # test_bruteforce.cpp:138-148 / acceptance C9
+    R = oracle.uniform_f32(40, 4, 56)
+    Q = oracle.uniform_f32(30, 4, 55)
+    for k in (1, 20, 40):
+        st = knn.SearchStats()
+        knn.bf_knn(Q, R, k, config=knn.BfConfig(count_distance_evals=True), stats=st)
+        assert st.distance_evals == 30 * 40
+    st = knn.SearchStats(distance_evals=123)
+    knn.bf_knn(Q, R, 3, stats=st)
+    assert st.distance_evals == 0  # bruteforce.cpp:98 writes 0 when not counting
+
+
+def test_sharded_merge_equals_single_search(knn, oracle):
+    """R split into shards with global index bases, merged on device ==
+    one search over all of R, bitwise (SURVEY.md 8(e) determinism)."""
+    import torch
+    m, d, n, k = 30000, 48, 800, 20
+    R = oracle.uniform_f32(m, d, 5)
+    Q = oracle.uniform_f32(n, d, 6)
+    full = knn.bf_knn(Q, R, k)
+    dev = torch.device("cuda:0")
+    Qd = torch.from_numpy(Q).to(dev)
+    bounds = [0, 7000, 19000, 30000]
+    keys = torch.empty((3, n, k), dtype=torch.float32, device=dev)
+    idxs = torch.empty((3, n, k), dtype=torch.int64, device=dev)
+    for s in range(3):
+        Rs = torch.from_numpy(R[bounds[s]:bounds[s + 1]].copy()).to(dev)
+        ix = knn.Index(device_ptr=Rs.data_ptr(), m=Rs.shape[0], d=d, index_base=bounds[s])
+        ix.search_device(Qd.data_ptr(), n, k, keys[s].data_ptr(), idxs[s].data_ptr(),
+                         raw_keys=True)
+        torch.cuda.synchronize()
+        ix.close()
+    od = torch.empty((n, k), dtype=torch.float32, device=dev)
+    oi = torch.empty((n, k), dtype=torch.int64, device=dev)
+    knn.merge_device(keys.data_ptr(), idxs.data_ptr(), 3, n, k, od.data_ptr(), oi.data_ptr())
+    torch.cuda.synchronize()
+    assert (oi.cpu().numpy() == full.index).all()
+    assert (od.cpu().numpy() == full.distance).all()
+
+
+def test_index_handle_host_roundtrip(knn, oracle):
+    R = oracle.uniform_f32(5000, 20, 21)
+    Q = oracle.uniform_f32(333, 20, 22)
+    ix = knn.Index(R)
+    a = ix.search(Q, 9)
+    b = knn.bf_knn(Q, R, 9)
+    assert (a.index == b.index).all() and (a.distance == b.distance).all()
+    ix.close()
+
+
+def test_large_d_and_odd_shapes(knn, oracle):
+    for (n, m, d, k) in [(1, 1, 1, 1), (65, 129, 300, 129), (3, 5000, 513, 7), (130, 64, 2, 64)]:
+        Q = oracle.uniform_f32(n, d, 1000 + d) * 3 - 1
+        R = oracle.uniform_f32(m, d, 2000 + d) * 3 - 1
+        ri, rd = oracle.knn(Q, R, k)
+        for path in PATHS:
+            t = knn.bf_knn(Q, R, k, config=cfg(knn, path))
+            rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+            assert rep.ok, f"{(n, m, d, k)} {path}: {rep}"
