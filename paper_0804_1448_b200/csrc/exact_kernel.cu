@@ -139,10 +139,11 @@ __global__ void __launch_bounds__(THREADS) exact_knn_kernel(ExactArgs a) {
         const int64_t q = q0 + row;
         if (q >= a.n) break;
         const size_t base = (static_cast<size_t>(split) * a.n + q) * a.k;
+        if (a.finalize) finalize_list(Lk + row * a.k, Li + row * a.k, a.k, M, lane);
         for (int t = lane; t < a.k; t += 32) {
             const float key = Lk[row * a.k + t];
             const int32_t li = Li[row * a.k + t];
-            a.out_key[base + t] = a.finalize ? finalize_key<M>(key) : key;
+            a.out_key[base + t] = key;
             a.out_idx[base + t] = li == 0x7fffffff ? kSentinelIdx : a.index_base + li;
         }
     }

@@ -71,9 +71,9 @@ __global__ void __launch_bounds__(WARPS * 32) merge_kernel(MergeArgs a) {
         }
     }
     __syncwarp();
+    if (a.finalize) finalize_list(lk, li, k, a.metric, lane);
     for (int t = lane; t < k; t += 32) {
-        const float key = lk[t];
-        a.out_key[q * k + t] = a.finalize ? finalize_key_rt(a.metric, key) : key;
+        a.out_key[q * k + t] = lk[t];
         a.out_idx[q * k + t] = li[t];
     }
 }

@@ -121,4 +121,29 @@ struct WarpList {
     }
 };
 
+// Finalize a sorted list in place (sqrt for L2) and restore the reference's
+// table invariant (test_bruteforce.cpp:22-39: equal reported distances appear
+// in ascending index order).  Two distinct squared keys can round to the same
+// sqrtf, so after finalization a run of equal distances may hold indices out
+// of order; keys were ascending, so runs are contiguous and short and one
+// lane's insertion pass fixes them in O(k + inversions).
+template <typename IdxT>
+__device__ void finalize_list(float* key, IdxT* idx, int k, int metric, int lane) {
+    for (int t = lane; t < k; t += 32) key[t] = finalize_key_rt(metric, key[t]);
+    __syncwarp();
+    if (metric == kL2 && lane == 0) {
+        for (int t = 1; t < k; ++t) {
+            const float v = key[t];
+            const IdxT j = idx[t];
+            int u = t;
+            while (u > 0 && key[u - 1] == v && idx[u - 1] > j) {
+                idx[u] = idx[u - 1];
+                --u;
+            }
+            idx[u] = j;
+        }
+    }
+    __syncwarp();
+}
+
 }  // namespace knnb200
