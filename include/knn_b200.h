@@ -161,6 +161,16 @@ KNN_B200_API void knn_b200_profile_enable(int on);
 KNN_B200_API int knn_b200_profile_collect(char *names, size_t names_len, double *ms,
                                           uint64_t *counts, int max_kernels);
 
+/* Tensor path diagnostics: how many queries of the last search on `device`
+ * (-1 = current) failed the candidate certificate and were recomputed by the
+ * exact kernel (results are identical either way). */
+KNN_B200_API int knn_b200_last_fallback_count(int device);
+
+/* Test hook: D[128x128] fp32 = A[128xK] * B[128xK]^T for fp16 device
+ * matrices through the engine's TMA / tcgen05 / TMEM primitives. */
+KNN_B200_API knn_b200_status knn_b200_debug_mma_probe(const void *d_a, const void *d_b, int32_t K,
+                                                      float *d_out);
+
 /* Synthetic uniform [0,1) FP32 on the device: element i of the stream is
  * splitmix64(seed + offset + i) >> 40 scaled by 2^-24 (host-reproducible). */
 KNN_B200_API knn_b200_status knn_b200_fill_uniform_device(float *d_out, int64_t count,

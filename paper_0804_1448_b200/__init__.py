@@ -39,6 +39,7 @@ EXPORTS = [
     "knn_b200_index_search", "knn_b200_index_search_device", "knn_b200_index_destroy",
     "knn_b200_merge_device", "knn_b200_launch_count", "knn_b200_reset_launch_count",
     "knn_b200_profile_enable", "knn_b200_profile_collect", "knn_b200_fill_uniform_device",
+    "knn_b200_last_fallback_count", "knn_b200_debug_mma_probe",
 ]
 
 
@@ -99,6 +100,8 @@ def library() -> C.CDLL:
     lib.knn_b200_profile_collect.restype = C.c_int
     lib.knn_b200_profile_collect.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_double),
                                              C.POINTER(C.c_uint64), C.c_int]
+    lib.knn_b200_last_fallback_count.restype = C.c_int
+    lib.knn_b200_last_fallback_count.argtypes = [C.c_int]
     lib.knn_b200_fill_uniform_device.restype = C.c_int
     lib.knn_b200_fill_uniform_device.argtypes = [vp, i64, C.c_uint64, i64, vp]
     for name in ("knn_b200_search", "knn_b200_search_device", "knn_b200_index_create",
@@ -115,6 +118,11 @@ def launch_count() -> int:
 
 def reset_launch_count() -> None:
     library().knn_b200_reset_launch_count()
+
+
+def last_fallback_count(device: int = -1) -> int:
+    """Queries of the last tensor-path search that failed certification."""
+    return int(library().knn_b200_last_fallback_count(device))
 
 
 def profile_enable(on: bool = True) -> None:

@@ -365,6 +365,14 @@ knn_b200_status knn_b200_index_search_device(knn_b200_index* index, const float*
 
 void knn_b200_index_destroy(knn_b200_index* index) { delete index; }
 
+int knn_b200_last_fallback_count(int device) {
+    try {
+        return context_for(device).last_fallbacks;
+    } catch (...) {
+        return -1;
+    }
+}
+
 knn_b200_status knn_b200_merge_device(const float* d_part_keys, const int64_t* d_part_idx,
                                       int32_t parts, int64_t n, int32_t k, int32_t metric,
                                       void* stream, float* d_out_dist, int64_t* d_out_idx) {

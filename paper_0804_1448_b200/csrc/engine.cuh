@@ -50,6 +50,7 @@ struct DeviceContext {
     DeviceArena arena;       // per-search scratch
     DeviceArena io;          // host-API staging of inputs / outputs
     std::mutex mu;           // one search at a time per context
+    int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
 };
 
 DeviceContext& context_for(int device);  // device < 0: current device

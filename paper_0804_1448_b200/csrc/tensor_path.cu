@@ -1,15 +1,998 @@
-// tensor_path.cu -- placeholder until the tcgen05 candidate kernel lands.
+// tensor_path.cu -- tcgen05 candidate generation + exact FP32 re-rank (L2).
+//
+// Replaces the reference's distance fill + selection (paths relative to
+// /root/reference/proj: src/bruteforce.cpp:23-38,81-96, include/knn/metric.hpp:22-29,
+// src/topk.cpp:17-33) for the Euclidean metric with a GEMM-form filter on
+// the 5th-generation tensor cores followed by an exact re-rank:
+//
+//  1. prep      Q, R -> centred, power-of-two-scaled fp16 copies (K-major rows,
+//               K padded to 16) with the squared norm of every rounded
+//               reference folded into three extra K columns (fp16 hi/mid/lo),
+//               so one tcgen05.mma chain yields  A = ||r~||^2 - 2 q~.r~  directly.
+//               Per point it also records delta = ||x~ - (x-mu)s|| (the
+//               rounding radius) for the certificate.
+//  2. filter    persistent, warp-specialised kernel: TMA producer warp,
+//               single-thread MMA issuer (M=128 queries x N=128 references x
+//               K, fp32 accumulators in 4 TMEM buffers), 8 epilogue warps
+//               (thread = query row of the 32x32b TMEM load) that scan the
+//               accumulators with FMNMX3 group minima against a per-query
+//               running threshold and keep a sorted candidate list of the
+//               K' = k+8 smallest A.  Work is split stream-K style so every
+//               SM gets the same number of 128x128 tiles.
+//  3. re-rank   warp per query: merge the candidate lists, derive the rigorous
+//               inclusion bound tau from the k-th smallest A,
+//               recompute the exact FP32 key of every candidate with A <= tau
+//               (key_step<kL2>, bitwise the exact kernel's arithmetic) and keep
+//               the exact top-k under the (key, index) order.
+//  4. fallback  queries whose certificate fails (a candidate list overflowed
+//               inside the bound: heavy near-ties/duplicates) are recomputed by
+//               the exact SIMT kernel.  Results are therefore bitwise identical
+//               to the exact path.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 #include "engine.cuh"
+#include "exact_kernel.cuh"
+#include "profile.cuh"
+#include "sm100.cuh"
 #include "tensor_path.cuh"
+#include "tmap.cuh"
+#include "warp_list.cuh"
 
 namespace knnb200 {
 
-bool tensor_path_supported(int64_t, int64_t, int, int) { return false; }
+namespace {
 
-void run_tensor_path(DeviceContext&, cudaStream_t, const float*, int64_t, const float*, int64_t,
-                     int, int, int, int64_t, float*, int64_t*) {
-    throw CudaError("tensor path not built");
+constexpr int TILE = 128;          // queries per MMA tile (M) and references per tile (N)
+constexpr int EPI_WARPS = 8;       // two groups of four (one warp per TMEM lane quarter)
+constexpr int EPI_THREADS = EPI_WARPS * 32;
+constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
+constexpr int NBUF = 4;            // TMEM accumulator buffers (4 x 128 columns = 512)
+constexpr int CAP = 4;             // group-buffer slots per epilogue thread
+constexpr int KEXTRA = 8;          // candidate list K' = k + KEXTRA
+constexpr int MAX_KQ = 32;
+constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
+
+struct Consts {         // per-query constants of the inclusion bound
+    float nq;           // ||q~||^2
+    float delta;        // delta_q + max_j delta_r
+    float eps;          // accumulation error bound of A
+    float c1;           // sqrt((1+rho)/(1-rho)), rounded up
+};
+
+// Rigorous inclusion threshold on A = ||r~||^2 - 2 q~.r~ given the k-th
+// smallest A seen so far.  Any reference whose exact FP32
+// key can still reach the final top-k has A <= thresh(A_k).  Rounded up.
+__device__ __forceinline__ float thresh(float ak, const Consts& c) {
+    const float u = sqrtf(fmaxf(ak + c.eps + c.nq, 0.f)) * (1.f + 1e-6f);
+    const float v = c.c1 * (u + c.delta) + c.delta;
+    const float t = v * v * (1.f + 4e-6f) - c.nq + c.eps;
+    return t + fabsf(t) * 4e-6f + 1e-30f;
+}
+
+struct PrepArgs {
+    const float* X;     // rows x d
+    int64_t rows, rows_pad;
+    int d, Kp;
+    int norm_col;       // first of three folded-norm columns, -1 if not folded
+    const float* mu;    // d
+    const float* scale; // 1
+    __half* Xh;         // rows_pad x Kp
+    float* norm;        // refs, no-fold: ||r~||^2 per row (+inf padding)
+    float4* qconst;     // queries: {nq, delta_q, ||q~||, 0}
+    unsigned* gmax;     // refs: [0] max delta_r bits, [1] max ||r~|| bits
+};
+
+// ordered-uint encoding of floats for atomicMin/Max over signed values
+__device__ __forceinline__ unsigned enc(float f) {
+    const unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float dec(unsigned u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// per-dimension min / max over the rows of X (both point sets)
+__global__ void range_kernel(const float* X, int64_t rows, int d, unsigned* mn, unsigned* mx) {
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int64_t r1 = min(rows, r0 + 64);
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float lo = kInf, hi = -kInf;
+        for (int64_t r = r0; r < r1; ++r) {
+            const float v = __ldg(X + r * d + c);
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+        if (r1 > r0) {
+            atomicMin(mn + c, enc(lo));
+            atomicMax(mx + c, enc(hi));
+        }
+    }
+}
+
+// centre mu_c = midrange, scale s = 2^e with max|x - mu| * s <= min(8, sqrt(30000/Kp))
+__global__ void scale_kernel(const unsigned* mn, const unsigned* mx, int d, int Kp, float* mu,
+                             float* scale, unsigned* gmax) {
+    __shared__ float red[256];
+    float m = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        const float lo = dec(mn[c]), hi = dec(mx[c]);
+        const float mc = 0.5f * (lo + hi);
+        mu[c] = mc;
+        m = fmaxf(m, fmaxf(fabsf(hi - mc), fabsf(mc - lo)));
+    }
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const float M = red[0] * (1.f + 1e-5f);
+        const float lim = fminf(8.f, sqrtf(30000.f / static_cast<float>(Kp)));
+        float s = 1.f;
+        if (M > 0.f && isfinite(M)) {
+            int e;
+            frexpf(lim / M, &e);  // lim/M = f * 2^e, f in [0.5, 1)
+            s = ldexpf(1.f, e - 1);
+        }
+        *scale = s;
+        gmax[0] = 0u;
+        gmax[1] = 0u;
+    }
+}
+
+// warp per row: fp16 conversion, folded norm, rounding radius
+template <bool QUERY>
+__global__ void convert_kernel(PrepArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= a.rows_pad) return;
+    const float s = *a.scale;
+    const bool real = row < a.rows;
+    double h2 = 0.0, e2 = 0.0;
+    __half* out = a.Xh + row * a.Kp;
+    for (int c = lane; c < a.Kp; c += 32) {
+        __half h = __float2half_rn(0.f);
+        if (real && c < a.d) {
+            const float t = __fsub_rn(__ldg(a.X + row * a.d + c), a.mu[c]) * s;
+            h = __float2half_rn(t);
+            const double hv = static_cast<double>(__half2float(h));
+            // fp16 rounding + the fp32 subtraction's rounding (<= 2^-24 |t|, doubled)
+            const double err = fabs(hv - static_cast<double>(t)) + fabs(static_cast<double>(t)) * 0x1.0p-23;
+            h2 += hv * hv;
+            e2 += err * err;
+            if (QUERY) h = __float2half_rn(-2.f * __half2float(h));  // exact: power-of-two scale
+        }
+        out[c] = h;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const float delta = static_cast<float>(sqrt(e2) * (1.0 + 0x1.0p-20)) * (1.f + 1e-6f);
+        const float xn = static_cast<float>(sqrt(h2)) * (1.f + 1e-6f);
+        if (QUERY) {
+            if (a.norm_col >= 0)
+                for (int j = 0; j < 3; ++j) out[a.norm_col + j] = __float2half_rn(1.f);
+            a.qconst[row] = make_float4(static_cast<float>(h2), delta, xn, 0.f);
+        } else {
+            if (a.norm_col >= 0) {
+                if (real) {
+                    const __half p1 = __double2half(h2);
+                    const double r1 = h2 - static_cast<double>(__half2float(p1));
+                    const __half p2 = __double2half(r1);
+                    const double r2 = r1 - static_cast<double>(__half2float(p2));
+                    out[a.norm_col] = p1;
+                    out[a.norm_col + 1] = p2;
+                    out[a.norm_col + 2] = __double2half(r2);
+                } else {
+                    out[a.norm_col] = __float2half_rn(kInf);
+                }
+            } else {
+                a.norm[row] = real ? static_cast<float>(h2) : kInf;
+            }
+            if (real) {
+                atomicMax(a.gmax + 0, __float_as_uint(delta));
+                atomicMax(a.gmax + 1, __float_as_uint(xn));
+            }
+        }
+    }
+}
+
+struct FilterArgs {
+    int64_t n, m;
+    int qtiles, rtiles;
+    int64_t U;             // qtiles * rtiles work units (128x128 tiles)
+    int G;                 // CTAs
+    int S_max;             // partial-list slots per query tile
+    int KB;                // 64-wide K blocks
+    int nslices;           // K / 16 MMA slices
+    int stages;
+    int k, Kq;
+    int d;
+    float gamma;           // accumulation error factor
+    float c1;
+    bool fold;
+    const float4* qconst;
+    const float* rnorm;    // no-fold norms
+    const unsigned* gmax;
+    unsigned* tglob;       // [n_pad] shared running threshold (ordered-uint, atomicMin)
+    float* part_A;         // [parts][Kq][128]
+    int* part_I;
+    int* part_cnt;         // [parts][128]
+    float* part_ev;        // [parts][128]
+};
+
+__device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
+    return (U * c) / G;
+}
+
+__device__ __forceinline__ int first_cta_of(int64_t u0, int64_t U, int G) {
+    int c = static_cast<int>((u0 * G) / U);
+    while (c + 1 < G && unit_start(U, G, c + 1) <= u0) ++c;
+    while (c > 0 && unit_start(U, G, c) > u0) --c;
+    return c;
+}
+
+__device__ __forceinline__ Consts load_consts(const FilterArgs& a, int64_t q) {
+    const float4 qc = a.qconst[q];
+    const float dr = __uint_as_float(a.gmax[0]);
+    const float rn = __uint_as_float(a.gmax[1]);
+    Consts c;
+    c.nq = qc.x;
+    c.delta = (qc.y + dr) * (1.f + 1e-6f);
+    // |A - (||r~||^2 - 2 q~.r~)| <= gamma * (2 ||q~|| ||r~|| + ||r~||^2)  (+ norm rounding
+    // when the norm is added in fp32 instead of folded)
+    const float mag = 2.f * qc.z * rn + rn * rn;
+    c.eps = a.gamma * mag + (a.fold ? 0.f : 0x1.0p-22f * mag) + 1e-30f;
+    c.c1 = a.c1;
+    return c;
+}
+
+__device__ __forceinline__ float min3(float x, float y, float z) {
+    float w;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(w) : "f"(x), "f"(y), "f"(z));
+    return w;
+}
+
+constexpr int BUFSLOTS = 40;   // per-lane candidate buffer; drained when > 8 after a 32-column chunk
+
+// Per-query candidate state of one epilogue thread: the KR smallest A seen by
+// this (CTA segment, epilogue group), sorted ascending, in registers.
+template <int KR>
+struct RegList {
+    float key[KR];
+    int idx[KR];
+    int cnt;
+    float evict;  // smallest A ever dropped for capacity (certificate input)
+
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int s = 0; s < KR; ++s) {
+            key[s] = kInf;
+            idx[s] = 0x7fffffff;
+        }
+        cnt = 0;
+        evict = kInf;
+    }
+    // branch-free compare-swap insertion chain (no dynamic register indexing)
+    __device__ __forceinline__ void insert(float x, int xi) {
+#pragma unroll
+        for (int s = 0; s < KR; ++s) {
+            const bool sw = x < key[s];
+            const float tk = sw ? key[s] : x;
+            const int ti = sw ? idx[s] : xi;
+            key[s] = sw ? x : key[s];
+            idx[s] = sw ? xi : idx[s];
+            x = tk;
+            xi = ti;
+        }
+        evict = fminf(evict, x);  // +inf while the list is not full
+        cnt = min(cnt + 1, KR);
+    }
+    __device__ __forceinline__ float kth(int k) const {
+        float v = kInf;
+#pragma unroll
+        for (int s = 0; s < KR; ++s)
+            if (s == k - 1) v = key[s];
+        return v;
+    }
+};
+
+template <int KR>
+__global__ void __launch_bounds__(THREADS, 1)
+    filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                  FilterArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
+    unsigned char* As = base;
+    unsigned char* Bs = base + KBB;
+    float* BA = reinterpret_cast<float*>(Bs + a.stages * KBB);   // [BUFSLOTS][256]
+    int* BI = reinterpret_cast<int*>(BA + BUFSLOTS * EPI_THREADS);  // [BUFSLOTS][256]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(BI + BUFSLOTS * EPI_THREADS);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + a.stages;
+    uint64_t* a_full = bars + 2 * a.stages;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* tfull = a_full + 2;
+    uint64_t* tempty = tfull + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int64_t u_begin = unit_start(a.U, a.G, cta);
+    const int64_t u_end = unit_start(a.U, a.G, cta + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            sm100::mbar_init(full + s, 1);
+            sm100::mbar_init(empty + s, 1);
+        }
+        sm100::mbar_init(a_full, 1);
+        sm100::mbar_init(a_empty, 1);
+        for (int b = 0; b < NBUF; ++b) {
+            sm100::mbar_init(tfull + b, 1);
+            sm100::mbar_init(tempty + b, 4);
+        }
+        sm100::fence_mbar_init();
+    }
+    if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer ----
+        if (sm100::elect_one()) {
+            sm100::tma_prefetch(&tq);
+            sm100::tma_prefetch(&tr);
+            int stage = 0;
+            uint32_t phase = 0, a_par = 0;
+            int cur_qt = -1;
+            for (int64_t u = u_begin; u < u_end; ++u) {
+                const int qt = static_cast<int>(u / a.rtiles);
+                const int rt = static_cast<int>(u % a.rtiles);
+                if (qt != cur_qt) {
+                    if (cur_qt >= 0) {
+                        sm100::mbar_wait(a_empty, a_par);
+                        a_par ^= 1u;
+                    }
+                    sm100::mbar_expect_tx(a_full, static_cast<uint32_t>(KBB));
+                    for (int kb = 0; kb < a.KB; ++kb)
+                        sm100::tma_load_2d(As + kb * 16384, &tq, a_full, kb * 64, qt * TILE);
+                    cur_qt = qt;
+                }
+                sm100::mbar_wait(empty + stage, phase ^ 1u);
+                sm100::mbar_expect_tx(full + stage, static_cast<uint32_t>(KBB));
+                unsigned char* dst = Bs + stage * KBB;
+                for (int kb = 0; kb < a.KB; ++kb)
+                    sm100::tma_load_2d(dst + kb * 16384, &tr, full + stage, kb * 64, rt * TILE);
+                if (++stage == a.stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA issuer -----
+        if (sm100::elect_one()) {
+            const uint32_t idesc = sm100::idesc_f16_f32(TILE, TILE);
+            int stage = 0;
+            uint32_t phase = 0, a_par = 0;
+            int cur_qt = -1;
+            int64_t t = 0;
+            for (int64_t u = u_begin; u < u_end; ++u, ++t) {
+                const int qt = static_cast<int>(u / a.rtiles);
+                if (qt != cur_qt) {
+                    if (cur_qt >= 0) sm100::mma_commit(a_empty);
+                    sm100::mbar_wait(a_full, a_par);
+                    a_par ^= 1u;
+                    cur_qt = qt;
+                }
+                const int b = static_cast<int>(t % NBUF);
+                sm100::mbar_wait(tempty + b, static_cast<uint32_t>((t / NBUF) & 1) ^ 1u);
+                sm100::mbar_wait(full + stage, phase);
+                sm100::tc_fence_after();
+                const uint32_t a0 = sm100::smem_u32(As);
+                const uint32_t b0 = sm100::smem_u32(Bs + stage * KBB);
+                const uint32_t dt = tmem + static_cast<uint32_t>(b * TILE);
+                for (int ks = 0; ks < a.nslices; ++ks) {
+                    const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
+                    sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off),
+                                      sm100::sdesc_k_sw128(b0 + off), idesc, ks > 0 ? 1u : 0u);
+                }
+                sm100::mma_commit(empty + stage);
+                sm100::mma_commit(tfull + b);
+                if (++stage == a.stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------- epilogue -------
+        const int ew = warp - 4;          // 0..7
+        const int grp = ew >> 2;          // tiles t with t % 2 == grp
+        const int quarter = warp & 3;     // TMEM lane quarter
+        const int et = ew * 32 + lane;    // buffer column (0..255)
+        const int row = quarter * 32 + lane;
+        const int k = a.k;
+
+        RegList<KR> L;
+        L.reset();
+        int cur_qt = -1;
+        int nb = 0;        // buffered candidates
+        float T = kInf;    // own bound: thresh(k-th smallest A of this list)
+        float Tf = kInf;   // filter bound: min(T, other group's, other CTAs')
+        Consts qc{};
+        int64_t q = 0;
+        int64_t t = 0;
+
+        auto drain = [&]() {
+            const int mx = __reduce_max_sync(0xffffffffu, nb);
+            for (int j = 0; j < mx; ++j) {
+                if (j < nb) {
+                    const float x = BA[j * EPI_THREADS + et];
+                    if (x < Tf) L.insert(x, BI[j * EPI_THREADS + et]);
+                }
+            }
+            nb = 0;
+            if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));
+            // share bounds through the per-query global slot: every part's bound
+            // is >= the final one, so the minimum over parts is a valid filter
+            if (T < kInf) atomicMin(a.tglob + q, enc(T));
+            Tf = fminf(T, fminf(kInf, dec(a.tglob[q])));
+        };
+
+        auto flush = [&](int qt) {
+            const int64_t u0 = static_cast<int64_t>(qt) * a.rtiles;
+            const int slot = cta - first_cta_of(u0, a.U, a.G);
+            const int64_t part = (static_cast<int64_t>(qt) * a.S_max + slot) * 2 + grp;
+            float* pa = a.part_A + part * a.Kq * TILE;
+            int* pi = a.part_I + part * a.Kq * TILE;
+#pragma unroll
+            for (int e = 0; e < KR; ++e) {
+                if (e < L.cnt) {
+                    pa[e * TILE + row] = L.key[e];
+                    pi[e * TILE + row] = L.idx[e];
+                }
+            }
+            a.part_cnt[part * TILE + row] = L.cnt;
+            a.part_ev[part * TILE + row] = L.evict;
+        };
+
+        for (int64_t u = u_begin; u < u_end; ++u, ++t) {
+            const int qt = static_cast<int>(u / a.rtiles);
+            const int rt = static_cast<int>(u % a.rtiles);
+            if ((t & 1) != grp) continue;
+            if (qt != cur_qt) {
+                if (cur_qt >= 0) {
+                    drain();
+                    flush(cur_qt);
+                }
+                cur_qt = qt;
+                q = static_cast<int64_t>(qt) * TILE + row;
+                qc = load_consts(a, q);
+                L.reset();
+                T = kInf;
+                Tf = fminf(kInf, dec(a.tglob[q]));  // memset 0xff reads as NaN -> +inf
+                nb = 0;
+            }
+            const int b = static_cast<int>(t % NBUF);
+            sm100::mbar_wait(tfull + b, static_cast<uint32_t>((t / NBUF) & 1));
+            sm100::tc_fence_after();
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                   static_cast<uint32_t>(b * TILE);
+            const int col_base = rt * TILE;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                sm100::tmem_ld_wait();
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                if (!a.fold) {
+                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 w = __ldg(nr + j);
+                        v[4 * j] += w.x;
+                        v[4 * j + 1] += w.y;
+                        v[4 * j + 2] += w.z;
+                        v[4 * j + 3] += w.w;
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const int o = g * 4;
+                    const float gm = fminf(min3(v[o], v[o + 1], v[o + 2]), v[o + 3]);
+                    if (gm < Tf) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            if (v[o + e] < Tf) {
+                                BA[nb * EPI_THREADS + et] = v[o + e];
+                                BI[nb * EPI_THREADS + et] = col_base + c * 32 + o + e;
+                                ++nb;
+                            }
+                        }
+                    }
+                }
+                // <= 8 buffered before the chunk, <= 32 appended: capacity 40
+                if (__any_sync(0xffffffffu, nb > 8)) drain();
+            }
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tempty + b);
+        }
+        if (cur_qt >= 0) {
+            drain();
+            flush(cur_qt);
+        }
+    }
+
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, 512);
+    }
+}
+
+// -------------------------------------------------------------- re-rank ----
+struct RerankArgs {
+    const float* Q;        // original fp32 n x d
+    const float* R;        // original fp32 m x d
+    int64_t n;
+    int d, k, Kq, S_max;
+    int rtiles;
+    FilterArgs f;          // constants + partial lists
+    int raw_keys;
+    int64_t index_base;
+    float* out;
+    int64_t* out_idx;
+    int* fb_count;
+    int* fb_list;
+};
+
+constexpr int RR_WARPS = 4;
+
+__global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * RR_WARPS + warp;
+    if (q >= a.n) return;
+    const int k = a.k;
+    const int Kq = a.Kq;
+    const int parts = a.S_max * 2;  // <= 32 (checked on the host)
+    const int span = parts * Kq;
+    // per-warp staging: candidate A / index of every partial list, exact list
+    float* sA = reinterpret_cast<float*>(smem_raw) + warp * span;
+    int* sI = reinterpret_cast<int*>(reinterpret_cast<float*>(smem_raw) + RR_WARPS * span) +
+              warp * span;
+    float* fk = reinterpret_cast<float*>(smem_raw) + 2 * RR_WARPS * span + warp * k;
+    int64_t* fi = reinterpret_cast<int64_t*>(reinterpret_cast<float*>(smem_raw) +
+                                             2 * RR_WARPS * span + RR_WARPS * k) +
+                  warp * k;  // byte offset 16*(2*span + k): 8-B aligned
+
+    const int qt = static_cast<int>(q / TILE);
+    const int row = static_cast<int>(q % TILE);
+    const int64_t p0 = static_cast<int64_t>(qt) * parts;
+
+    int cnt = 0;
+    float ev = kInf;
+    if (lane < parts) {
+        cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
+        ev = a.f.part_ev[(p0 + lane) * TILE + row];
+    }
+    // 0. stage every list (independent loads, one round trip)
+    for (int x = lane; x < span; x += 32) {
+        const int p = x / Kq, e = x - p * Kq;
+        float va = kInf;
+        int vi = 0x7fffffff;
+        const int64_t part = p0 + p;
+        if (e < a.f.part_cnt[part * TILE + row]) {
+            va = a.f.part_A[(part * Kq + e) * TILE + row];
+            vi = a.f.part_I[(part * Kq + e) * TILE + row];
+        }
+        sA[x] = va;
+        sI[x] = vi;
+    }
+    __syncwarp();
+
+    // 1. k-th smallest A over all lists: k-step tournament on the sorted list heads
+    int head = 0;
+    float hv = (lane < parts && cnt > 0) ? sA[lane * Kq] : kInf;
+    float ak = kInf;
+    for (int s = 0; s < k; ++s) {
+        float mv = hv;
+        int ml = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, ml, o);
+            if (ov < mv || (ov == mv && ol < ml)) {
+                mv = ov;
+                ml = ol;
+            }
+        }
+        ak = mv;
+        if (lane == ml) {
+            ++head;
+            hv = head < cnt ? sA[lane * Kq + head] : kInf;
+        }
+    }
+    const Consts qc = load_consts(a.f, q);
+    const float tau = thresh(ak, qc);
+
+    // 2. certificate: nothing within tau was ever dropped for capacity
+    const bool ok = __all_sync(0xffffffffu, cnt == 0 || ev > tau) && isfinite(tau);
+    if (!ok) {
+        if (lane == 0) {
+            const int slot = atomicAdd(a.fb_count, 1);
+            a.fb_list[slot] = static_cast<int>(q);
+        }
+        return;
+    }
+
+    // 3. candidates with A <= tau, exact FP32 keys, exact top-k
+    WarpList<int64_t> LF{fk, fi, k};
+    LF.init(lane);
+    __syncwarp();
+    const float* qrow = a.Q + q * a.d;
+    int taken = 0;   // candidates consumed so far (warp-uniform)
+    int myj = -1;    // reference index of this lane's pending candidate
+    // exact keys of the pending candidates (lane-parallel), then offer them
+    auto emit = [&]() {
+        float key = kInf;
+        int64_t gid = kSentinelIdx;
+        if (myj >= 0) {
+            const float* rrow = a.R + static_cast<int64_t>(myj) * a.d;
+            float acc = 0.f;
+            if ((a.d & 3) == 0) {
+                const float4* q4 = reinterpret_cast<const float4*>(qrow);
+                const float4* r4 = reinterpret_cast<const float4*>(rrow);
+#pragma unroll 4
+                for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
+                    const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
+                    acc = key_step<kL2>(acc, u.x, w.x);
+                    acc = key_step<kL2>(acc, u.y, w.y);
+                    acc = key_step<kL2>(acc, u.z, w.z);
+                    acc = key_step<kL2>(acc, u.w, w.w);
+                }
+            } else {
+                for (int cc = 0; cc < a.d; ++cc)
+                    acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
+            }
+            key = acc;
+            gid = myj;
+        }
+        float ck[1] = {key};
+        int64_t ci[1] = {gid};
+        LF.offer<1>(ck, ci, lane);
+        myj = -1;
+    };
+    for (int x0 = 0; x0 < span; x0 += 32) {
+        const int x = x0 + lane;
+        const bool c = x < span && sA[x] <= tau;
+        const unsigned bal = __ballot_sync(0xffffffffu, c);
+        const int pos = taken + __popc(bal & ((1u << lane) - 1u));
+        const int j = c ? sI[x] : -1;
+        unsigned rem = bal;
+        while (rem) {
+            const int src = __ffs(rem) - 1;
+            rem &= rem - 1;
+            const int pj = __shfl_sync(0xffffffffu, j, src);
+            const int pp = __shfl_sync(0xffffffffu, pos, src);
+            if ((pp & 31) == lane) myj = pj;
+            if ((pp & 31) == 31) emit();  // 32 candidates assembled
+        }
+        taken += __popc(bal);
+    }
+    if (taken & 31) emit();
+    __syncwarp();
+    if (!a.raw_keys) finalize_list(fk, fi, k, kL2, lane);
+    for (int t = lane; t < k; t += 32) {
+        a.out[q * k + t] = fk[t];
+        a.out_idx[q * k + t] = a.index_base + fi[t];
+    }
+}
+
+// gather / scatter for the certification fallback
+__global__ void gather_rows_kernel(const float* X, int d, const int* list, int count, float* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(count) * d;
+    if (i >= total) return;
+    const int64_t r = i / d;
+    out[i] = X[static_cast<int64_t>(list[r]) * d + i % d];
+}
+
+__global__ void scatter_rows_kernel(const float* src_d, const int64_t* src_i, const int* list,
+                                    int count, int k, float* out, int64_t* out_idx) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(count) * k) return;
+    const int64_t r = i / k;
+    const int64_t dst = static_cast<int64_t>(list[r]) * k + i % k;
+    out[dst] = src_d[i];
+    out_idx[dst] = src_i[i];
+}
+
+struct Layout {
+    int d16, Kp, KB, norm_col, stages, Kq;
+    bool fold;
+    size_t smem;
+};
+
+Layout layout_for(int d, int k) {
+    Layout L{};
+    L.d16 = (d + 15) / 16 * 16;
+    // candidate list size = the register-list template size (16 / 24 / 32)
+    const int want = std::min(k + KEXTRA, MAX_KQ);
+    L.Kq = want <= 16 ? 16 : (want <= 24 ? 24 : 32);
+    const int kb_plain = (L.d16 + 63) / 64;
+    int kfold, ncol;
+    if (L.d16 - d >= 3) {
+        kfold = L.d16;
+        ncol = d;
+    } else {
+        kfold = L.d16 + 16;
+        ncol = L.d16;
+    }
+    const int kb_fold = (kfold + 63) / 64;
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * BUFSLOTS * 8;
+    const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
+    auto stages_for = [&](int KB) {
+        const size_t per = static_cast<size_t>(KB) * 16384;
+        const long avail = static_cast<long>(SMEM_LIMIT) - static_cast<long>(fixed + per);
+        return avail > 0 ? static_cast<int>(avail / static_cast<long>(per)) : 0;
+    };
+    if (kb_fold == kb_plain || stages_for(kb_fold) >= 3) {
+        L.fold = true;
+        L.Kp = kfold;
+        L.KB = kb_fold;
+        L.norm_col = ncol;
+    } else {
+        L.fold = false;
+        L.Kp = L.d16;
+        L.KB = kb_plain;
+        L.norm_col = -1;
+    }
+    L.stages = std::min(stages_for(L.KB), 6);
+    L.smem = fixed + static_cast<size_t>(L.KB) * 16384 * (1 + L.stages);
+    return L;
+}
+
+}  // namespace
+
+bool tensor_path_supported(int64_t n, int64_t m, int d, int k) {
+    if (d < 1 || d > 128 || k < 1 || k + KEXTRA > MAX_KQ) return false;
+    if (m < k || n < 1 || m > (1LL << 30)) return false;
+    return layout_for(d, k).stages >= 2;
+}
+
+void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                     const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
+                     float* d_out, int64_t* d_idx) {
+    const Layout L = layout_for(d, k);
+    const int qtiles = static_cast<int>((n + TILE - 1) / TILE);
+    const int rtiles = static_cast<int>((m + TILE - 1) / TILE);
+    const int64_t n_pad = static_cast<int64_t>(qtiles) * TILE;
+    const int64_t m_pad = static_cast<int64_t>(rtiles) * TILE;
+    const int64_t U = static_cast<int64_t>(qtiles) * rtiles;
+    // at most ~14 CTAs share a query tile, so a query has <= 32 partial lists
+    const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
+                                                     static_cast<int64_t>(qtiles) * 14));
+    // partial-list slots per query tile under the stream-K split
+    int S_max = 1;
+    for (int qt = 0; qt < qtiles; ++qt) {
+        const int64_t u0 = static_cast<int64_t>(qt) * rtiles, u1 = u0 + rtiles - 1;
+        const int c0 = static_cast<int>((u0 * G) / U), c1 = static_cast<int>((u1 * G) / U);
+        S_max = std::max(S_max, c1 - c0 + 3);  // +2 slack for floor rounding at the ends
+    }
+    if (S_max > 16) throw CudaError("tensor path: too many partial lists per query tile");
+    const int64_t parts = static_cast<int64_t>(qtiles) * S_max * 2;
+
+    Sizer sz;
+    sz.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
+    sz.take<__half>(static_cast<size_t>(m_pad) * L.Kp);
+    sz.take<float>(static_cast<size_t>(m_pad));
+    sz.take<float4>(static_cast<size_t>(n_pad));
+    sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
+    sz.take<float>(static_cast<size_t>(d) + 1);
+    sz.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
+    sz.take<int>(static_cast<size_t>(parts) * L.Kq * TILE);
+    sz.take<int>(static_cast<size_t>(parts) * TILE);
+    sz.take<float>(static_cast<size_t>(parts) * TILE);
+    sz.take<int>(static_cast<size_t>(n) + 1);
+    sz.take<unsigned>(static_cast<size_t>(n_pad));
+    ctx.arena.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.arena.base())};
+    __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
+    __half* Rh = cv.take<__half>(static_cast<size_t>(m_pad) * L.Kp);
+    float* rnorm = cv.take<float>(static_cast<size_t>(m_pad));
+    float4* qconst = cv.take<float4>(static_cast<size_t>(n_pad));
+    unsigned* mnmx = cv.take<unsigned>(2 * static_cast<size_t>(d) + 2);
+    float* mu = cv.take<float>(static_cast<size_t>(d) + 1);
+    float* part_A = cv.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
+    int* part_I = cv.take<int>(static_cast<size_t>(parts) * L.Kq * TILE);
+    int* part_cnt = cv.take<int>(static_cast<size_t>(parts) * TILE);
+    float* part_ev = cv.take<float>(static_cast<size_t>(parts) * TILE);
+    int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
+    unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
+    unsigned* gmax = mnmx + 2 * d;
+    float* scale = mu + d;
+
+    // 1. prep
+    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx, 0xff, sizeof(unsigned) * d, stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx + d, 0x00, sizeof(unsigned) * d, stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
+    {
+        ProfileScope ps(stream, "prep_range_kernel");
+        range_kernel<<<static_cast<unsigned>((m + 63) / 64), 128, 0, stream>>>(dR, m, d, mnmx,
+                                                                                mnmx + d);
+        range_kernel<<<static_cast<unsigned>((n + 63) / 64), 128, 0, stream>>>(dQ, n, d, mnmx,
+                                                                                mnmx + d);
+    }
+    KNN_LAUNCH_CHECK();
+    note_launch();
+    {
+        ProfileScope ps(stream, "prep_scale_kernel");
+        scale_kernel<<<1, 256, 0, stream>>>(mnmx, mnmx + d, d, L.Kp, mu, scale, gmax);
+    }
+    KNN_LAUNCH_CHECK();
+    PrepArgs pr{};
+    pr.d = d;
+    pr.Kp = L.Kp;
+    pr.norm_col = L.fold ? L.norm_col : -1;
+    pr.mu = mu;
+    pr.scale = scale;
+    pr.gmax = gmax;
+    pr.X = dR;
+    pr.rows = m;
+    pr.rows_pad = m_pad;
+    pr.Xh = Rh;
+    pr.norm = rnorm;
+    {
+        ProfileScope ps(stream, "prep_convert_refs");
+        convert_kernel<false><<<static_cast<unsigned>((m_pad + 7) / 8), 256, 0, stream>>>(pr);
+    }
+    KNN_LAUNCH_CHECK();
+    pr.X = dQ;
+    pr.rows = n;
+    pr.rows_pad = n_pad;
+    pr.Xh = Qh;
+    pr.qconst = qconst;
+    {
+        ProfileScope ps(stream, "prep_convert_queries");
+        convert_kernel<true><<<static_cast<unsigned>((n_pad + 7) / 8), 256, 0, stream>>>(pr);
+    }
+    KNN_LAUNCH_CHECK();
+
+    // 2. tcgen05 filter
+    FilterArgs fa{};
+    fa.n = n;
+    fa.m = m;
+    fa.qtiles = qtiles;
+    fa.rtiles = rtiles;
+    fa.U = U;
+    fa.G = G;
+    fa.S_max = S_max;
+    fa.KB = L.KB;
+    fa.nslices = L.Kp / 16;
+    fa.stages = L.stages;
+    fa.k = k;
+    fa.Kq = L.Kq;
+    fa.d = d;
+    // <= (slices + 4) roundings of 2^-23 relative to sum |terms| each, doubled
+    fa.gamma = static_cast<float>((fa.nslices + 4) * std::ldexp(1.0, -21));
+    const double rho = (d + 8) * std::ldexp(1.0, -24);
+    fa.c1 = static_cast<float>(std::sqrt((1 + rho) / (1 - rho)) * (1 + 1e-6));
+    fa.fold = L.fold;
+    fa.qconst = qconst;
+    fa.rnorm = rnorm;
+    fa.gmax = gmax;
+    fa.tglob = tglob;
+    fa.part_A = part_A;
+    fa.part_I = part_I;
+    fa.part_cnt = part_cnt;
+    fa.part_ev = part_ev;
+    const CUtensorMap tq = make_tmap_f16_sw128(Qh, n_pad, L.Kp, TILE, 64);
+    const CUtensorMap tr = make_tmap_f16_sw128(Rh, m_pad, L.Kp, TILE, 64);
+    auto launch_filter = [&](auto kern) {
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(L.smem)));
+        ProfileScope ps(stream, "tc_filter_kernel");
+        kern<<<G, THREADS, L.smem, stream>>>(tq, tr, fa);
+    };
+    if (L.Kq == 16)
+        launch_filter(filter_kernel<16>);
+    else if (L.Kq == 24)
+        launch_filter(filter_kernel<24>);
+    else
+        launch_filter(filter_kernel<32>);
+    KNN_LAUNCH_CHECK();
+
+    // 3. exact re-rank
+    RerankArgs ra{};
+    ra.Q = dQ;
+    ra.R = dR;
+    ra.n = n;
+    ra.d = d;
+    ra.k = k;
+    ra.Kq = L.Kq;
+    ra.S_max = S_max;
+    ra.rtiles = rtiles;
+    ra.f = fa;
+    ra.raw_keys = raw_keys;
+    ra.index_base = index_base;
+    ra.out = d_out;
+    ra.out_idx = d_idx;
+    ra.fb_count = fb;
+    ra.fb_list = fb + 1;
+    const size_t rr_smem =
+        static_cast<size_t>(RR_WARPS) * (2 * 4 * S_max * 2 * L.Kq + static_cast<size_t>(k) * 12) + 16;
+    {
+        ProfileScope ps(stream, "rerank_kernel");
+        rerank_kernel<<<static_cast<unsigned>((n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, rr_smem,
+                        stream>>>(ra);
+    }
+    KNN_LAUNCH_CHECK();
+
+    // 4. certification fallback (exact kernel on the failed queries)
+    int fails = 0;
+    KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
+    if (fails > 0) {
+        std::vector<int> list(static_cast<size_t>(fails));
+        KNN_CUDA_CHECK(cudaMemcpy(list.data(), fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToHost));
+        // the fallback allocates its own scratch: keep the gathered queries in a
+        // dedicated buffer so the exact path's arena use cannot clobber them
+        float* gq = nullptr;
+        float* od = nullptr;
+        int64_t* oi = nullptr;
+        int* dl = nullptr;
+        KNN_CUDA_CHECK(cudaMallocAsync(&gq, sizeof(float) * fails * d, stream));
+        KNN_CUDA_CHECK(cudaMallocAsync(&od, sizeof(float) * fails * k, stream));
+        KNN_CUDA_CHECK(cudaMallocAsync(&oi, sizeof(int64_t) * fails * k, stream));
+        KNN_CUDA_CHECK(cudaMallocAsync(&dl, sizeof(int) * fails, stream));
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dl, list.data(), sizeof(int) * fails, cudaMemcpyHostToDevice,
+                                       stream));
+        {
+            const int64_t tot = static_cast<int64_t>(fails) * d;
+            ProfileScope ps(stream, "fallback_gather");
+            gather_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
+                dQ, d, dl, fails, gq);
+        }
+        KNN_LAUNCH_CHECK();
+        run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
+        {
+            const int64_t tot = static_cast<int64_t>(fails) * k;
+            ProfileScope ps(stream, "fallback_scatter");
+            scatter_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
+                od, oi, dl, fails, k, d_out, d_idx);
+        }
+        KNN_LAUNCH_CHECK();
+        KNN_CUDA_CHECK(cudaFreeAsync(gq, stream));
+        KNN_CUDA_CHECK(cudaFreeAsync(od, stream));
+        KNN_CUDA_CHECK(cudaFreeAsync(oi, stream));
+        KNN_CUDA_CHECK(cudaFreeAsync(dl, stream));
+    }
+    ctx.last_fallbacks = fails;
 }
 
 }  // namespace knnb200

@@ -240,3 +240,25 @@ def test_large_d_and_odd_shapes(knn, oracle):
             t = knn.bf_knn(Q, R, k, config=cfg(knn, path))
             rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
             assert rep.ok, f"{(n, m, d, k)} {path}: {rep}"
+
+
+def test_tensor_path_is_used_and_certified(knn, oracle):
+    """Random data: every query certified by the tcgen05 candidate bound (no
+    exact-kernel fallback); duplicate-heavy data: certificate fails, fallback
+    recomputes, results still exact."""
+    R = oracle.uniform_f32(20000, 96, 31)
+    Q = oracle.uniform_f32(3000, 96, 32)
+    t = knn.bf_knn(Q, R, 20, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() == 0
+    ri, rd = oracle.knn(Q[:300], R, 20)
+    assert compare(t.index[:300], t.distance[:300], ri, rd, Q[:300], R, oracle=oracle).ok
+    # 40 copies of every point: > K' candidates inside the bound -> fallback
+    base = oracle.uniform_f32(100, 16, 33)
+    Rd = np.repeat(base, 40, axis=0)
+    Qd = oracle.uniform_f32(50, 16, 34)
+    td = knn.bf_knn(Qd, Rd, 20, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() > 0
+    te = knn.bf_knn(Qd, Rd, 20, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (td.index == te.index).all() and (td.distance == te.distance).all()
+    ri, rd = oracle.knn(Qd, Rd, 20)
+    assert compare(td.index, td.distance, ri, rd, Qd, Rd, oracle=oracle).ok
