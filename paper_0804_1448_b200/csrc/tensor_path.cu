@@ -53,7 +53,7 @@ constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
 constexpr int NBUF = 4;            // TMEM accumulator buffers (4 x 128 columns = 512)
 constexpr int CAP = 4;             // group-buffer slots per epilogue thread
-constexpr int KEXTRA = 8;          // candidate list K' = k + KEXTRA
+constexpr int KEXTRA = 0;          // candidate list K' >= k + KEXTRA
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
 
@@ -225,6 +225,8 @@ struct FilterArgs {
     const float* rnorm;    // no-fold norms
     const unsigned* gmax;
     unsigned* tglob;       // [n_pad] shared running threshold (ordered-uint, atomicMin)
+    float* pub;            // [n_pad][2*S_max] per-part published ceil(k/P)-th smallest A
+    int pmax;              // 2*S_max
     float* part_A;         // [parts][Kq][128]
     int* part_I;
     int* part_cnt;         // [parts][128]
@@ -287,12 +289,12 @@ struct RegList {
     __device__ __forceinline__ void insert(float x, int xi) {
 #pragma unroll
         for (int s = 0; s < KR; ++s) {
-            const bool sw = x < key[s];
-            const float tk = sw ? key[s] : x;
+            const bool sw = x < key[s];           // strict: ties keep stream order
+            const float lo = fminf(x, key[s]);
+            x = fmaxf(x, key[s]);
+            key[s] = lo;
             const int ti = sw ? idx[s] : xi;
-            key[s] = sw ? x : key[s];
             idx[s] = sw ? xi : idx[s];
-            x = tk;
             xi = ti;
         }
         evict = fminf(evict, x);  // +inf while the list is not full
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         sm100::mbar_init(a_empty, 1);
         for (int b = 0; b < NBUF; ++b) {
             sm100::mbar_init(tfull + b, 1);
-            sm100::mbar_init(tempty + b, 4);
+            sm100::mbar_init(tempty + b, EPI_WARPS);
         }
         sm100::fence_mbar_init();
     }
@@ -361,9 +363,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0, a_par = 0;
             int cur_qt = -1;
+            int qt = static_cast<int>(u_begin / a.rtiles);
+            int rt = static_cast<int>(u_begin % a.rtiles);
             for (int64_t u = u_begin; u < u_end; ++u) {
-                const int qt = static_cast<int>(u / a.rtiles);
-                const int rt = static_cast<int>(u % a.rtiles);
                 if (qt != cur_qt) {
                     if (cur_qt >= 0) {
                         sm100::mbar_wait(a_empty, a_par);
@@ -383,6 +385,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     stage = 0;
                     phase ^= 1u;
                 }
+                if (++rt == a.rtiles) {
+                    rt = 0;
+                    ++qt;
+                }
             }
         }
     } else if (warp == 1) {
@@ -393,8 +399,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t phase = 0, a_par = 0;
             int cur_qt = -1;
             int64_t t = 0;
+            int qt = static_cast<int>(u_begin / a.rtiles);
+            int rt = static_cast<int>(u_begin % a.rtiles);
             for (int64_t u = u_begin; u < u_end; ++u, ++t) {
-                const int qt = static_cast<int>(u / a.rtiles);
                 if (qt != cur_qt) {
                     if (cur_qt >= 0) sm100::mma_commit(a_empty);
                     sm100::mbar_wait(a_full, a_par);
@@ -419,12 +426,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                     stage = 0;
                     phase ^= 1u;
                 }
+                if (++rt == a.rtiles) {
+                    rt = 0;
+                    ++qt;
+                }
             }
         }
     } else if (warp >= 4) {
         // ------------------------------------------------- epilogue -------
         const int ew = warp - 4;          // 0..7
-        const int grp = ew >> 2;          // tiles t with t % 2 == grp
+        const int grp = ew >> 2;          // column half of every tile
         const int quarter = warp & 3;     // TMEM lane quarter
         const int et = ew * 32 + lane;    // buffer column (0..255)
         const int row = quarter * 32 + lane;
@@ -440,6 +451,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int64_t q = 0;
         int64_t t = 0;
 
+        int nparts = 2, kp = k, my_part = grp;  // parts of the current query tile
         auto drain = [&]() {
             const int mx = __reduce_max_sync(0xffffffffu, nb);
             for (int j = 0; j < mx; ++j) {
@@ -450,10 +462,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             nb = 0;
             if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));
-            // share bounds through the per-query global slot: every part's bound
-            // is >= the final one, so the minimum over parts is a valid filter
+            // (1) own bound, shared as a per-query minimum (each part's bound is
+            //     >= the final one)
             if (T < kInf) atomicMin(a.tglob + q, enc(T));
-            Tf = fminf(T, fminf(kInf, dec(a.tglob[q])));
+            float tf = fminf(T, fminf(kInf, dec(a.tglob[q])));
+            // (2) union bound: if every one of the P parts holds ceil(k/P) values
+            //     <= v_p, the union holds >= k values <= max_p v_p, so
+            //     A_(k) <= max_p v_p and thresh(max_p v_p) is a valid filter.
+            float* pq = a.pub + q * a.pmax;
+            if (L.cnt >= kp) pq[my_part] = L.kth(kp);
+            float u = -kInf;
+            for (int p = 0; p < nparts; ++p) u = fmaxf(u, pq[p]);
+            if (u < 1e38f) tf = fminf(tf, thresh(u, qc));
+            Tf = tf;
         };
 
         auto flush = [&](int qt) {
@@ -473,10 +494,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             a.part_ev[part * TILE + row] = L.evict;
         };
 
+        int qt = static_cast<int>(u_begin / a.rtiles);
+        int rt = static_cast<int>(u_begin % a.rtiles);
         for (int64_t u = u_begin; u < u_end; ++u, ++t) {
-            const int qt = static_cast<int>(u / a.rtiles);
-            const int rt = static_cast<int>(u % a.rtiles);
-            if ((t & 1) != grp) continue;
             if (qt != cur_qt) {
                 if (cur_qt >= 0) {
                     drain();
@@ -489,6 +509,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 T = kInf;
                 Tf = fminf(kInf, dec(a.tglob[q]));  // memset 0xff reads as NaN -> +inf
                 nb = 0;
+                const int64_t u0 = static_cast<int64_t>(qt) * a.rtiles;
+                const int c0 = first_cta_of(u0, a.U, a.G);
+                const int c1 = first_cta_of(u0 + a.rtiles - 1, a.U, a.G);
+                nparts = 2 * (c1 - c0 + 1);
+                kp = (k + nparts - 1) / nparts;
+                my_part = 2 * (cta - c0) + grp;
             }
             const int b = static_cast<int>(t % NBUF);
             sm100::mbar_wait(tfull + b, static_cast<uint32_t>((t / NBUF) & 1));
@@ -497,7 +523,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                    static_cast<uint32_t>(b * TILE);
             const int col_base = rt * TILE;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 2 * grp; c < 2 * grp + 2; ++c) {
                 uint32_t r[32];
                 sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
                 sm100::tmem_ld_wait();
@@ -536,6 +562,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + b);
+            if (++rt == a.rtiles) {
+                rt = 0;
+                ++qt;
+            }
         }
         if (cur_qt >= 0) {
             drain();
@@ -739,9 +769,18 @@ struct Layout {
 Layout layout_for(int d, int k) {
     Layout L{};
     L.d16 = (d + 15) / 16 * 16;
-    // candidate list size = the register-list template size (16 / 24 / 32)
+    // candidate list size = the register-list template size >= k.  Each query
+    // has >= 2 partial lists and only ~k+3 candidates inside the final bound
+    // (measured, tools/margin_stats.py), so a list of k overflows inside the
+    // bound only in near-tie-heavy data -- which the certificate catches.
     const int want = std::min(k + KEXTRA, MAX_KQ);
-    L.Kq = want <= 16 ? 16 : (want <= 24 ? 24 : 32);
+    static const int sizes[] = {4, 8, 12, 16, 20, 24, 32};
+    L.Kq = 32;
+    for (int sz : sizes)
+        if (sz >= want) {
+            L.Kq = sz;
+            break;
+        }
     const int kb_plain = (L.d16 + 63) / 64;
     int kfold, ncol;
     if (L.d16 - d >= 3) {
@@ -818,6 +857,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<float>(static_cast<size_t>(parts) * TILE);
     sz.take<int>(static_cast<size_t>(n) + 1);
     sz.take<unsigned>(static_cast<size_t>(n_pad));
+    sz.take<float>(static_cast<size_t>(n_pad) * 2 * S_max);
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -832,6 +872,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     float* part_ev = cv.take<float>(static_cast<size_t>(parts) * TILE);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
+    float* pub = cv.take<float>(static_cast<size_t>(n_pad) * 2 * S_max);
     unsigned* gmax = mnmx + 2 * d;
     float* scale = mu + d;
 
@@ -841,6 +882,8 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
+    // 0x7f7f7f7f = 3.4e38: "not yet published"
+    KNN_CUDA_CHECK(cudaMemsetAsync(pub, 0x7f, sizeof(float) * n_pad * 2 * S_max, stream));
     {
         ProfileScope ps(stream, "prep_range_kernel");
         range_kernel<<<static_cast<unsigned>((m + 63) / 64), 128, 0, stream>>>(dR, m, d, mnmx,
@@ -907,6 +950,8 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.rnorm = rnorm;
     fa.gmax = gmax;
     fa.tglob = tglob;
+    fa.pub = pub;
+    fa.pmax = 2 * S_max;
     fa.part_A = part_A;
     fa.part_I = part_I;
     fa.part_cnt = part_cnt;
@@ -919,12 +964,15 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         ProfileScope ps(stream, "tc_filter_kernel");
         kern<<<G, THREADS, L.smem, stream>>>(tq, tr, fa);
     };
-    if (L.Kq == 16)
-        launch_filter(filter_kernel<16>);
-    else if (L.Kq == 24)
-        launch_filter(filter_kernel<24>);
-    else
-        launch_filter(filter_kernel<32>);
+    switch (L.Kq) {
+        case 4: launch_filter(filter_kernel<4>); break;
+        case 8: launch_filter(filter_kernel<8>); break;
+        case 12: launch_filter(filter_kernel<12>); break;
+        case 16: launch_filter(filter_kernel<16>); break;
+        case 20: launch_filter(filter_kernel<20>); break;
+        case 24: launch_filter(filter_kernel<24>); break;
+        default: launch_filter(filter_kernel<32>); break;
+    }
     KNN_LAUNCH_CHECK();
 
     // 3. exact re-rank
