@@ -141,6 +141,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(inside)}
 
 
+def measured_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from
+    the newest committed ncu --set full summary (profiles/r*_traffic.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            table = json.load(f)
+    except Exception:
+        return None
+    key = kernel.replace("tc_", "").replace("_glist", "")
+    for name, val in table.items():
+        if key in name:
+            return {"bytes_per_launch": int(val), "source": os.path.relpath(files[-1], ROOT)}
+    return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -172,7 +191,9 @@ def run_ours(args):
     Q = torch.empty((n, d), dtype=torch.float32, device=dev)
     knn.fill_uniform_device(R.data_ptr(), m * d, sr, 0, sptr)
     knn.fill_uniform_device(Q.data_ptr(), n * d, sq, 0, sptr)
-    lo, hi = rank * m // world, (rank + 1) * m // world
+    from paper_0804_1448_b200.sharding import check_shardable, shard_bounds
+    check_shardable(m, world, k)
+    lo, hi = shard_bounds(m, world, rank)
     Rs = R[lo:hi]
     index = knn.Index(device_ptr=Rs.data_ptr(), m=hi - lo, d=d, index_base=lo, device=local)
     out_d = torch.empty((n, k), dtype=torch.float32, device=dev)
@@ -252,7 +273,7 @@ def run_ours(args):
         peak = peaks["bf16_tflops"]
         achieved = alg / (per_launch_ms / 1e3) / 1e12
     roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": peak, "unit": unit,
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": measured_traffic(dom_name),
                 "kernel": dom_name, "per_launch_ms": round(per_launch_ms, 4),
                 "launches": dom_cnt, "peak_source": f"{peak_src} (MEASURED_PEAKS.json bf16 dense)"
                 if bound == "tensor" else f"{peak_src} (MEASURED_PEAKS.json hbm)",
