@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -52,7 +54,6 @@ constexpr int EPI_WARPS = 8;       // two groups of four (one warp per TMEM lane
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
 constexpr int NBUF = 4;            // TMEM accumulator buffers (4 x 128 columns = 512)
-constexpr int CAP = 4;             // group-buffer slots per epilogue thread
 constexpr int KEXTRA = 0;          // candidate list K' >= k + KEXTRA
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
@@ -94,6 +95,10 @@ __device__ __forceinline__ unsigned enc(float f) {
 }
 __device__ __forceinline__ float dec(unsigned u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+// 0xffffffff (memset "no bound yet") decodes as NaN: map it to +inf
+__device__ __forceinline__ float dec_or_inf(unsigned u) {
+    return fminf(kInf, dec(u));
 }
 
 // per-dimension min / max over the rows of X (both point sets)
@@ -231,6 +236,9 @@ struct FilterArgs {
     int* part_I;
     int* part_cnt;         // [parts][128]
     float* part_ev;        // [parts][128]
+    int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 1 ld+min, 2 no epilogue work
+    float* sink;
+    unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS): slow chunks, drains, steps, kept, tiles
 };
 
 __device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
@@ -259,13 +267,28 @@ __device__ __forceinline__ Consts load_consts(const FilterArgs& a, int64_t q) {
     return c;
 }
 
+// w[e] for a runtime e in [0, 8), as an opaque select chain (a plain dynamic
+// index would demote w to local memory)
+__device__ __forceinline__ float sel8(const float (&w)[8], int e) {
+    float x = w[0];
+#pragma unroll
+    for (int s = 1; s < 8; ++s)
+        asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\tselp.f32 %0, %1, %0, p;\n\t}"
+            : "+f"(x)
+            : "f"(w[s]), "r"(e), "r"(s));
+    return x;
+}
+
 __device__ __forceinline__ float min3(float x, float y, float z) {
     float w;
     asm("min.f32 %0, %1, %2, %3;" : "=f"(w) : "f"(x), "f"(y), "f"(z));
     return w;
 }
 
-constexpr int BUFSLOTS = 40;   // per-lane candidate buffer; drained when > 8 after a 32-column chunk
+constexpr int CAP = 8;         // per-lane buffered 8-column groups (smem planes [slot][thread])
+constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow, warpgroup 0 shrinks
+constexpr int CTRL_REGS = 40;
+
 
 // Per-query candidate state of one epilogue thread: the KR smallest A seen by
 // this (CTA segment, epilogue group), sorted ascending, in registers.
@@ -300,11 +323,16 @@ struct RegList {
         evict = fminf(evict, x);  // +inf while the list is not full
         cnt = min(cnt + 1, KR);
     }
+    // key[k-1] for a runtime k.  The select chain is opaque inline PTX: written
+    // as plain C++ the compiler turns it back into key[k-1], a dynamic index
+    // that demotes the whole list to local memory.
     __device__ __forceinline__ float kth(int k) const {
         float v = kInf;
 #pragma unroll
         for (int s = 0; s < KR; ++s)
-            if (s == k - 1) v = key[s];
+            asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\tselp.f32 %0, %1, %0, p;\n\t}"
+                : "+f"(v)
+                : "f"(key[s]), "r"(k - 1), "r"(s));
         return v;
     }
 };
@@ -319,9 +347,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
     unsigned char* As = base;
     unsigned char* Bs = base + KBB;
-    float* BA = reinterpret_cast<float*>(Bs + a.stages * KBB);   // [BUFSLOTS][256]
-    int* BI = reinterpret_cast<int*>(BA + BUFSLOTS * EPI_THREADS);  // [BUFSLOTS][256]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(BI + BUFSLOTS * EPI_THREADS);
+    // candidate groups: two float4 planes (values 0-3 / 4-7) + column base, [slot][thread]
+    float4* BA0 = reinterpret_cast<float4*>(Bs + a.stages * KBB);
+    float4* BA1 = BA0 + CAP * EPI_THREADS;
+    int* BI = reinterpret_cast<int*>(BA1 + CAP * EPI_THREADS);
+    uint64_t* sT = reinterpret_cast<uint64_t*>(BI + CAP * EPI_THREADS);  // [128] tagged bounds
+    uint64_t* sP = sT + TILE;                                           // [2][128] tagged kp-th A
+    uint64_t* bars = sP + 2 * TILE;
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
     uint64_t* a_full = bars + 2 * a.stages;
@@ -350,11 +382,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         sm100::fence_mbar_init();
     }
     if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
+    for (int i = threadIdx.x; i < 3 * TILE; i += blockDim.x) sT[i] = ~0ull;  // no tag matches
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
     if (warp == 0) {
         // ------------------------------------------------ TMA producer ----
         if (sm100::elect_one()) {
@@ -434,12 +468,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------- epilogue -------
+        sm100::reg_alloc<EPI_REGS>();
         const int ew = warp - 4;          // 0..7
         const int grp = ew >> 2;          // column half of every tile
         const int quarter = warp & 3;     // TMEM lane quarter
         const int et = ew * 32 + lane;    // buffer column (0..255)
         const int row = quarter * 32 + lane;
         const int k = a.k;
+        const int kp = (k + 1) >> 1;      // union bound: ceil(k/2) per column group
 
         RegList<KR> L;
         L.reset();
@@ -447,130 +483,188 @@ __global__ void __launch_bounds__(THREADS, 1)
         int nb = 0;        // buffered candidates
         float T = kInf;    // own bound: thresh(k-th smallest A of this list)
         float Tf = kInf;   // filter bound: min(T, other group's, other CTAs')
+        unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
         Consts qc{};
         int64_t q = 0;
         int64_t t = 0;
+        uint64_t tagT = 0, tagP = 0;     // segment tags of the smem bound exchange
+        unsigned long long st_slow = 0, st_hits = 0, st_drains = 0, st_steps = 0;
 
-        int nparts = 2, kp = k, my_part = grp;  // parts of the current query tile
-        auto drain = [&]() {
-            const int mx = __reduce_max_sync(0xffffffffu, nb);
-            for (int j = 0; j < mx; ++j) {
-                if (j < nb) {
-                    const float x = BA[j * EPI_THREADS + et];
-                    if (x < Tf) L.insert(x, BI[j * EPI_THREADS + et]);
-                }
-            }
-            nb = 0;
-            if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));
-            // (1) own bound, shared as a per-query minimum (each part's bound is
-            //     >= the final one)
-            if (T < kInf) atomicMin(a.tglob + q, enc(T));
-            float tf = fminf(T, fminf(kInf, dec(a.tglob[q])));
-            // (2) union bound: if every one of the P parts holds ceil(k/P) values
-            //     <= v_p, the union holds >= k values <= max_p v_p, so
-            //     A_(k) <= max_p v_p and thresh(max_p v_p) is a valid filter.
-            float* pq = a.pub + q * a.pmax;
-            if (L.cnt >= kp) pq[my_part] = L.kth(kp);
-            float u = -kInf;
-            for (int p = 0; p < nparts; ++p) u = fmaxf(u, pq[p]);
-            if (u < 1e38f) tf = fminf(tf, thresh(u, qc));
-            Tf = tf;
-        };
+        // Insert every buffered candidate still under the bound, then refresh
+        // the bound from (1) this list, (2) the other column group's list of
+        // the same query (smem, tagged by segment), (3) the union of both
+        // groups' ceil(k/2)-th values, (4) other CTAs' parts of the query
+        // (global atomicMin, read one drain late so the load latency hides).
+#define KNN_DRAIN()                                                                              \
+    do {                                                                                         \
+        const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
+        if (a.stats) { ++st_drains; st_steps += mx_; st_slow += nb; }                            \
+        _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
+            if (j_ < nb) {                                                                       \
+                const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et];   \
+                const int c_ = BI[j_ * EPI_THREADS + et];                                        \
+                const float w_[8] = {p_.x, p_.y, p_.z, p_.w, q_.x, q_.y, q_.z, q_.w};            \
+                unsigned m_ = 0;                                                                 \
+                _Pragma("unroll") for (int e_ = 0; e_ < 8; ++e_) m_ |= (w_[e_] < Tf ? 1u : 0u) << e_; \
+                while (m_) { /* this lane's hits only: the warp runs max-popc rounds */          \
+                    const int e_ = __ffs(m_) - 1;                                                \
+                    m_ &= m_ - 1;                                                                \
+                    L.insert(sel8(w_, e_), c_ + e_);                                             \
+                }                                                                                \
+            }                                                                                    \
+        }                                                                                        \
+        nb = 0;                                                                                  \
+        if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
+        float tf_ = fminf(T, dec_or_inf(tg_pref));                                               \
+        if (T < kInf) {                                                                          \
+            atomicMin(a.tglob + q, enc(T));                                                      \
+            atomicMin(reinterpret_cast<unsigned long long*>(sT + row),                           \
+                      static_cast<unsigned long long>(tagT | enc(T)));                           \
+        }                                                                                        \
+        tg_pref = __ldcg(a.tglob + q);                                                           \
+        const uint64_t so_ = sT[row];                                                            \
+        if ((so_ & 0xffffffff00000000ull) == tagT) tf_ = fminf(tf_, dec(static_cast<unsigned>(so_))); \
+        if (L.cnt >= kp) {                                                                       \
+            const float mine_ = L.kth(kp);                                                       \
+            sP[grp * TILE + row] = tagP | enc(mine_);                                            \
+            const uint64_t po_ = sP[(grp ^ 1) * TILE + row];                                     \
+            if ((po_ & 0xffffffff00000000ull) == tagP)                                           \
+                tf_ = fminf(tf_, thresh(fmaxf(mine_, dec(static_cast<unsigned>(po_))), qc));     \
+        }                                                                                        \
+        Tf = tf_;                                                                                \
+    } while (0)
 
-        auto flush = [&](int qt) {
-            const int64_t u0 = static_cast<int64_t>(qt) * a.rtiles;
-            const int slot = cta - first_cta_of(u0, a.U, a.G);
-            const int64_t part = (static_cast<int64_t>(qt) * a.S_max + slot) * 2 + grp;
-            float* pa = a.part_A + part * a.Kq * TILE;
-            int* pi = a.part_I + part * a.Kq * TILE;
-#pragma unroll
-            for (int e = 0; e < KR; ++e) {
-                if (e < L.cnt) {
-                    pa[e * TILE + row] = L.key[e];
-                    pi[e * TILE + row] = L.idx[e];
-                }
-            }
-            a.part_cnt[part * TILE + row] = L.cnt;
-            a.part_ev[part * TILE + row] = L.evict;
-        };
+#define KNN_FLUSH(qt_)                                                                           \
+    do {                                                                                         \
+        const int64_t u0_ = static_cast<int64_t>(qt_) * a.rtiles;                                \
+        const int slot_ = cta - first_cta_of(u0_, a.U, a.G);                                    \
+        const int64_t part_ = (static_cast<int64_t>(qt_) * a.S_max + slot_) * 2 + grp;           \
+        float* pa_ = a.part_A + part_ * a.Kq * TILE;                                             \
+        int* pi_ = a.part_I + part_ * a.Kq * TILE;                                               \
+        _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_) {                                      \
+            if (e_ < L.cnt) {                                                                    \
+                pa_[e_ * TILE + row] = L.key[e_];                                                \
+                pi_[e_ * TILE + row] = L.idx[e_];                                                \
+            }                                                                                    \
+        }                                                                                        \
+        a.part_cnt[part_ * TILE + row] = L.cnt;                                                  \
+        a.part_ev[part_ * TILE + row] = L.evict;                                                 \
+    } while (0)
+
+        // One 32-column chunk, branch-free: the minimum of each 8-column group
+        // (FMNMX3), and every group whose minimum is under the lane's bound is
+        // appended whole (two 16-B stores + its column base) to the lane's
+        // buffer; the drain re-filters the 8 values.  A hit costs a few
+        // predicated stores instead of a divergent branch, which matters
+        // because with 32 queries per warp some lane hits in most chunks.
+#define KNN_SCAN_CHUNK(vv, colb)                                                                 \
+    do {                                                                                         \
+        if (__any_sync(0xffffffffu, nb > CAP - 4)) KNN_DRAIN();                                  \
+        _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                       \
+            const float* w_ = vv + 8 * i_;                                                       \
+            const float gm_ = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]),   \
+                                         w_[6]), w_[7]);                                         \
+            if (gm_ < Tf) {                                                                      \
+                BA0[nb * EPI_THREADS + et] = make_float4(w_[0], w_[1], w_[2], w_[3]);            \
+                BA1[nb * EPI_THREADS + et] = make_float4(w_[4], w_[5], w_[6], w_[7]);            \
+                BI[nb * EPI_THREADS + et] = (colb) + 8 * i_;                                     \
+                ++nb;                                                                            \
+            }                                                                                    \
+        }                                                                                        \
+    } while (0)
 
         int qt = static_cast<int>(u_begin / a.rtiles);
         int rt = static_cast<int>(u_begin % a.rtiles);
         for (int64_t u = u_begin; u < u_end; ++u, ++t) {
             if (qt != cur_qt) {
                 if (cur_qt >= 0) {
-                    drain();
-                    flush(cur_qt);
+                    KNN_DRAIN();
+                    KNN_FLUSH(cur_qt);
                 }
                 cur_qt = qt;
                 q = static_cast<int64_t>(qt) * TILE + row;
                 qc = load_consts(a, q);
                 L.reset();
                 T = kInf;
-                Tf = fminf(kInf, dec(a.tglob[q]));  // memset 0xff reads as NaN -> +inf
+                tg_pref = __ldcg(a.tglob + q);
+                Tf = dec_or_inf(tg_pref);
                 nb = 0;
-                const int64_t u0 = static_cast<int64_t>(qt) * a.rtiles;
-                const int c0 = first_cta_of(u0, a.U, a.G);
-                const int c1 = first_cta_of(u0 + a.rtiles - 1, a.U, a.G);
-                nparts = 2 * (c1 - c0 + 1);
-                kp = (k + nparts - 1) / nparts;
-                my_part = 2 * (cta - c0) + grp;
+                tagT = static_cast<uint64_t>(0x7fffffffu - static_cast<unsigned>(qt)) << 32;
+                tagP = static_cast<uint64_t>(qt) << 32;
             }
             const int b = static_cast<int>(t % NBUF);
             sm100::mbar_wait(tfull + b, static_cast<uint32_t>((t / NBUF) & 1));
             sm100::tc_fence_after();
             const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                   static_cast<uint32_t>(b * TILE);
-            const int col_base = rt * TILE;
-#pragma unroll 1
-            for (int c = 2 * grp; c < 2 * grp + 2; ++c) {
-                uint32_t r[32];
-                sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
+                                   static_cast<uint32_t>(b * TILE + grp * 64);
+            const int col_base = rt * TILE + grp * 64;
+            if (a.mode == 2) {
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + b);
+            } else {
+                uint32_t r0[32], r1[32];
+                sm100::tmem_ld_32x32b_x32(taddr, r0);
+                sm100::tmem_ld_32x32b_x32(taddr + 32, r1);
                 sm100::tmem_ld_wait();
-                float v[32];
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + b);  // registers hold the tile now
+                float v0[32], v1[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                for (int j = 0; j < 32; ++j) {
+                    v0[j] = __uint_as_float(r0[j]);
+                    v1[j] = __uint_as_float(r1[j]);
+                }
                 if (!a.fold) {
-                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base + c * 32);
+                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const float4 w = __ldg(nr + j);
-                        v[4 * j] += w.x;
-                        v[4 * j + 1] += w.y;
-                        v[4 * j + 2] += w.z;
-                        v[4 * j + 3] += w.w;
+                        const float4 w = __ldg(nr + j), w2 = __ldg(nr + 8 + j);
+                        v0[4 * j] += w.x;
+                        v0[4 * j + 1] += w.y;
+                        v0[4 * j + 2] += w.z;
+                        v0[4 * j + 3] += w.w;
+                        v1[4 * j] += w2.x;
+                        v1[4 * j + 1] += w2.y;
+                        v1[4 * j + 2] += w2.z;
+                        v1[4 * j + 3] += w2.w;
                     }
                 }
+                if (a.mode == 1) {
+                    float acc = kInf;
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    const int o = g * 4;
-                    const float gm = fminf(min3(v[o], v[o + 1], v[o + 2]), v[o + 3]);
-                    if (gm < Tf) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            if (v[o + e] < Tf) {
-                                BA[nb * EPI_THREADS + et] = v[o + e];
-                                BI[nb * EPI_THREADS + et] = col_base + c * 32 + o + e;
-                                ++nb;
-                            }
-                        }
-                    }
+                    for (int j = 0; j < 32; j += 2) acc = min3(acc, v0[j], v1[j + 1]);
+                    if (acc == -1.f) a.sink[0] = acc;
+                } else {
+                    KNN_SCAN_CHUNK(v0, col_base);
+                    KNN_SCAN_CHUNK(v1, col_base + 32);
                 }
-                // <= 8 buffered before the chunk, <= 32 appended: capacity 40
-                if (__any_sync(0xffffffffu, nb > 8)) drain();
             }
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tempty + b);
             if (++rt == a.rtiles) {
                 rt = 0;
                 ++qt;
             }
         }
         if (cur_qt >= 0) {
-            drain();
-            flush(cur_qt);
+            KNN_DRAIN();
+            KNN_FLUSH(cur_qt);
         }
+        if (a.stats) {
+            st_hits = 0;
+            const unsigned long long w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(L.cnt));
+            const unsigned long long pushed = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_slow));
+            if (lane == 0) {
+                atomicAdd(a.stats + 0, pushed);
+                atomicAdd(a.stats + 1, st_drains);
+                atomicAdd(a.stats + 2, st_steps);
+                atomicAdd(a.stats + 3, w + st_hits);
+                atomicAdd(a.stats + 4, static_cast<unsigned long long>(t));
+            }
+        }
+#undef KNN_SCAN_CHUNK
+#undef KNN_DRAIN
+#undef KNN_FLUSH
     }
 
     sm100::tc_fence_before();
@@ -791,7 +885,7 @@ Layout layout_for(int d, int k) {
         ncol = L.d16;
     }
     const int kb_fold = (kfold + 63) / 64;
-    const size_t epi = static_cast<size_t>(EPI_THREADS) * BUFSLOTS * 8;
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 36 + 3 * TILE * 8;
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
     auto stages_for = [&](int KB) {
         const size_t per = static_cast<size_t>(KB) * 16384;
@@ -956,6 +1050,13 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.part_I = part_I;
     fa.part_cnt = part_cnt;
     fa.part_ev = part_ev;
+    if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
+    fa.sink = part_ev;
+    const bool want_stats = std::getenv("KNN_B200_FILTER_STATS") != nullptr;
+    if (want_stats) {
+        KNN_CUDA_CHECK(cudaMallocAsync(&fa.stats, 8 * sizeof(unsigned long long), stream));
+        KNN_CUDA_CHECK(cudaMemsetAsync(fa.stats, 0, 8 * sizeof(unsigned long long), stream));
+    }
     const CUtensorMap tq = make_tmap_f16_sw128(Qh, n_pad, L.Kp, TILE, 64);
     const CUtensorMap tr = make_tmap_f16_sw128(Rh, m_pad, L.Kp, TILE, 64);
     auto launch_filter = [&](auto kern) {
@@ -974,6 +1075,18 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         default: launch_filter(filter_kernel<32>); break;
     }
     KNN_LAUNCH_CHECK();
+    if (want_stats) {
+        unsigned long long h[8];
+        KNN_CUDA_CHECK(cudaMemcpyAsync(h, fa.stats, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
+        KNN_CUDA_CHECK(cudaFree(fa.stats));
+        const double warps = static_cast<double>(G) * EPI_WARPS;
+        std::fprintf(stderr,
+                     "[filter stats] per warp: tiles %.1f groups-pushed/lane %.1f drains %.1f insert-steps "
+                     "%.1f | kept/list %.2f\n",
+                     h[4] / warps, h[0] / (warps * 32.0), h[1] / warps, h[2] / warps,
+                     h[3] / (warps * 32.0));
+    }
 
     // 3. exact re-rank
     RerankArgs ra{};
