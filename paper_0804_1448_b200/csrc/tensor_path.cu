@@ -215,7 +215,8 @@ __global__ void convert_kernel(PrepArgs a) {
 struct FilterArgs {
     int64_t n, m;
     int qtiles, rtiles;
-    int64_t U;             // qtiles * rtiles work units (128x128 tiles)
+    int pairs;             // query-tile pairs (a CTA keeps both tiles of a pair resident)
+    int64_t U;             // pairs * rtiles work units (one 128-reference tile x 256 queries)
     int G;                 // CTAs
     int S_max;             // partial-list slots per query tile
     int KB;                // 64-wide K blocks
@@ -230,15 +231,13 @@ struct FilterArgs {
     const float* rnorm;    // no-fold norms
     const unsigned* gmax;
     unsigned* tglob;       // [n_pad] shared running threshold (ordered-uint, atomicMin)
-    float* pub;            // [n_pad][2*S_max] per-part published ceil(k/P)-th smallest A
-    int pmax;              // 2*S_max
     float* part_A;         // [parts][Kq][128]
     int* part_I;
     int* part_cnt;         // [parts][128]
     float* part_ev;        // [parts][128]
     int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 1 ld+min, 2 no epilogue work
     float* sink;
-    unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS): slow chunks, drains, steps, kept, tiles
+    unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
 };
 
 __device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
@@ -285,13 +284,35 @@ __device__ __forceinline__ float min3(float x, float y, float z) {
     return w;
 }
 
-constexpr int CAP = 8;         // per-lane buffered 8-column groups (smem planes [slot][thread])
+constexpr int CAP = 6;         // per-lane buffered 8-column groups (smem planes [slot][thread])
 constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow, warpgroup 0 shrinks
 constexpr int CTRL_REGS = 40;
 
+// Predicated append of one 8-value group to a lane's smem candidate buffer:
+// stores happen iff gm < tf (inline PTX so the compiler cannot turn the
+// predicate into a branch).  a0/a1: the slot's two float4 plane addresses,
+// ai: its column-base address (shared window).
+__device__ __forceinline__ void push_group(float gm, float tf, uint32_t a0, uint32_t a1, uint32_t ai,
+                                           const float* w, int col) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %0, %1;\n\t"
+        "@p st.shared.v4.f32 [%2], {%5, %6, %7, %8};\n\t"
+        "@p st.shared.v4.f32 [%3], {%9, %10, %11, %12};\n\t"
+        "@p st.shared.b32 [%4], %13;\n\t}" ::"f"(gm),
+        "f"(tf), "r"(a0), "r"(a1), "r"(ai), "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]), "f"(w[4]),
+        "f"(w[5]), "f"(w[6]), "f"(w[7]), "r"(col)
+        : "memory");
+}
 
-// Per-query candidate state of one epilogue thread: the KR smallest A seen by
-// this (CTA segment, epilogue group), sorted ascending, in registers.
+// (a < b) ? if_lt : if_ge as one setp + selp (opaque: never a branch)
+__device__ __forceinline__ int sel_lt(float a, float b, int if_lt, int if_ge) {
+    int r;
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tselp.b32 %0, %3, %4, p;\n\t}"
+        : "=r"(r)
+        : "f"(a), "f"(b), "r"(if_lt), "r"(if_ge));
+    return r;
+}
+
 template <int KR>
 struct RegList {
     float key[KR];
@@ -309,18 +330,21 @@ struct RegList {
         evict = kInf;
     }
     // branch-free compare-swap insertion chain (no dynamic register indexing)
+    // Insert by rank, branch-free: slot s becomes max(key[s-1], min(x, key[s]))
+    // (= key[s-1] if x sorts before it, x if it lands here, else unchanged) and
+    // the index follows with two predicated selects.  Every slot depends only
+    // on x and the old list, so there is no serial chain; the selects are
+    // inline PTX because the compiler otherwise turns them into per-slot
+    // branches (ties: x goes after equal keys).
     __device__ __forceinline__ void insert(float x, int xi) {
+        evict = fminf(evict, fmaxf(x, key[KR - 1]));  // +inf while the list is not full
 #pragma unroll
-        for (int s = 0; s < KR; ++s) {
-            const bool sw = x < key[s];           // strict: ties keep stream order
-            const float lo = fminf(x, key[s]);
-            x = fmaxf(x, key[s]);
-            key[s] = lo;
-            const int ti = sw ? idx[s] : xi;
-            idx[s] = sw ? xi : idx[s];
-            xi = ti;
+        for (int s = KR - 1; s > 0; --s) {
+            idx[s] = sel_lt(x, key[s - 1], idx[s - 1], sel_lt(x, key[s], xi, idx[s]));
+            key[s] = fmaxf(key[s - 1], fminf(x, key[s]));
         }
-        evict = fminf(evict, x);  // +inf while the list is not full
+        idx[0] = sel_lt(x, key[0], xi, idx[0]);
+        key[0] = fminf(x, key[0]);
         cnt = min(cnt + 1, KR);
     }
     // key[k-1] for a runtime k.  The select chain is opaque inline PTX: written
@@ -337,30 +361,37 @@ struct RegList {
     }
 };
 
+// Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
+// resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA,
+// one thread of warp 1 issues two M=128 N=128 MMA chains per reference tile
+// (one per query tile, accumulators in 2 x 2 TMEM buffers), and epilogue
+// group g (4 warps, one per TMEM lane quarter) owns query tile g of the pair:
+// thread = query row, all 128 columns of every tile.  So each query keeps ONE
+// candidate list per CTA that touches it (not one per column split), and each
+// reference tile fetched from L2 feeds two MMAs.
 template <int KR>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
                   FilterArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 1024-B aligned start, derived by offset so the compiler keeps the shared
+    // address space (LDS/STS instead of generic accesses)
+    unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
-    unsigned char* As = base;
-    unsigned char* Bs = base + KBB;
+    unsigned char* As = base;                // 2 query tiles
+    unsigned char* Bs = base + 2 * KBB;      // stages x reference tile
     // candidate groups: two float4 planes (values 0-3 / 4-7) + column base, [slot][thread]
     float4* BA0 = reinterpret_cast<float4*>(Bs + a.stages * KBB);
     float4* BA1 = BA0 + CAP * EPI_THREADS;
     int* BI = reinterpret_cast<int*>(BA1 + CAP * EPI_THREADS);
-    uint64_t* sT = reinterpret_cast<uint64_t*>(BI + CAP * EPI_THREADS);  // [128] tagged bounds
-    uint64_t* sP = sT + TILE;                                           // [2][128] tagged kp-th A
-    uint64_t* bars = sP + 2 * TILE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(BI + CAP * EPI_THREADS);
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
     uint64_t* a_full = bars + 2 * a.stages;
     uint64_t* a_empty = a_full + 1;
-    uint64_t* tfull = a_full + 2;
-    uint64_t* tempty = tfull + NBUF;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+    uint64_t* tfull = a_full + 2;  // [group][buffer]
+    uint64_t* tempty = tfull + 4;  // [group][buffer]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -375,14 +406,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         sm100::mbar_init(a_full, 1);
         sm100::mbar_init(a_empty, 1);
-        for (int b = 0; b < NBUF; ++b) {
+        for (int b = 0; b < 4; ++b) {
             sm100::mbar_init(tfull + b, 1);
-            sm100::mbar_init(tempty + b, EPI_WARPS);
+            sm100::mbar_init(tempty + b, 4);
         }
         sm100::fence_mbar_init();
     }
     if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
-    for (int i = threadIdx.x; i < 3 * TILE; i += blockDim.x) sT[i] = ~0ull;  // no tag matches
     sm100::tc_fence_before();
     __syncthreads();
     sm100::tc_fence_after();
@@ -396,21 +426,23 @@ __global__ void __launch_bounds__(THREADS, 1)
             sm100::tma_prefetch(&tr);
             int stage = 0;
             uint32_t phase = 0, a_par = 0;
-            int cur_qt = -1;
-            int qt = static_cast<int>(u_begin / a.rtiles);
+            int cur_p = -1;
+            int p = static_cast<int>(u_begin / a.rtiles);
             int rt = static_cast<int>(u_begin % a.rtiles);
             for (int64_t u = u_begin; u < u_end; ++u) {
-                if (qt != cur_qt) {
-                    if (cur_qt >= 0) {
-                        sm100::mbar_wait(a_empty, a_par);
+                if (p != cur_p) {
+                    if (cur_p >= 0) {
+                        sm100::mbar_wait_sleep(a_empty, a_par);
                         a_par ^= 1u;
                     }
-                    sm100::mbar_expect_tx(a_full, static_cast<uint32_t>(KBB));
-                    for (int kb = 0; kb < a.KB; ++kb)
-                        sm100::tma_load_2d(As + kb * 16384, &tq, a_full, kb * 64, qt * TILE);
-                    cur_qt = qt;
+                    sm100::mbar_expect_tx(a_full, static_cast<uint32_t>(2 * KBB));
+                    for (int g = 0; g < 2; ++g)
+                        for (int kb = 0; kb < a.KB; ++kb)
+                            sm100::tma_load_2d(As + g * KBB + kb * 16384, &tq, a_full, kb * 64,
+                                               (2 * p + g) * TILE);
+                    cur_p = p;
                 }
-                sm100::mbar_wait(empty + stage, phase ^ 1u);
+                sm100::mbar_wait_sleep(empty + stage, phase ^ 1u);
                 sm100::mbar_expect_tx(full + stage, static_cast<uint32_t>(KBB));
                 unsigned char* dst = Bs + stage * KBB;
                 for (int kb = 0; kb < a.KB; ++kb)
@@ -421,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 if (++rt == a.rtiles) {
                     rt = 0;
-                    ++qt;
+                    ++p;
                 }
             }
         }
@@ -431,38 +463,42 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t idesc = sm100::idesc_f16_f32(TILE, TILE);
             int stage = 0;
             uint32_t phase = 0, a_par = 0;
-            int cur_qt = -1;
+            int cur_p = -1;
             int64_t t = 0;
-            int qt = static_cast<int>(u_begin / a.rtiles);
+            int p = static_cast<int>(u_begin / a.rtiles);
             int rt = static_cast<int>(u_begin % a.rtiles);
             for (int64_t u = u_begin; u < u_end; ++u, ++t) {
-                if (qt != cur_qt) {
-                    if (cur_qt >= 0) sm100::mma_commit(a_empty);
-                    sm100::mbar_wait(a_full, a_par);
+                if (p != cur_p) {
+                    if (cur_p >= 0) sm100::mma_commit(a_empty);
+                    sm100::mbar_wait_sleep(a_full, a_par);
                     a_par ^= 1u;
-                    cur_qt = qt;
+                    cur_p = p;
                 }
-                const int b = static_cast<int>(t % NBUF);
-                sm100::mbar_wait(tempty + b, static_cast<uint32_t>((t / NBUF) & 1) ^ 1u);
-                sm100::mbar_wait(full + stage, phase);
+                const int b = static_cast<int>(t & 1);
+                const uint32_t tpar = static_cast<uint32_t>((t >> 1) & 1);
+                sm100::mbar_wait_sleep(full + stage, phase);
                 sm100::tc_fence_after();
-                const uint32_t a0 = sm100::smem_u32(As);
                 const uint32_t b0 = sm100::smem_u32(Bs + stage * KBB);
-                const uint32_t dt = tmem + static_cast<uint32_t>(b * TILE);
-                for (int ks = 0; ks < a.nslices; ++ks) {
-                    const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
-                    sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off),
-                                      sm100::sdesc_k_sw128(b0 + off), idesc, ks > 0 ? 1u : 0u);
+                for (int g = 0; g < 2; ++g) {
+                    sm100::mbar_wait_sleep(tempty + 2 * g + b, tpar ^ 1u);
+                    sm100::tc_fence_after();
+                    const uint32_t a0 = sm100::smem_u32(As + g * KBB);
+                    const uint32_t dt = tmem + static_cast<uint32_t>((2 * g + b) * TILE);
+                    for (int ks = 0; ks < a.nslices; ++ks) {
+                        const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
+                        sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off),
+                                          sm100::sdesc_k_sw128(b0 + off), idesc, ks > 0 ? 1u : 0u);
+                    }
+                    sm100::mma_commit(tfull + 2 * g + b);
                 }
                 sm100::mma_commit(empty + stage);
-                sm100::mma_commit(tfull + b);
                 if (++stage == a.stages) {
                     stage = 0;
                     phase ^= 1u;
                 }
                 if (++rt == a.rtiles) {
                     rt = 0;
-                    ++qt;
+                    ++p;
                 }
             }
         }
@@ -470,75 +506,75 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ------------------------------------------------- epilogue -------
         sm100::reg_alloc<EPI_REGS>();
         const int ew = warp - 4;          // 0..7
-        const int grp = ew >> 2;          // column half of every tile
+        const int grp = ew >> 2;          // query tile of the pair
         const int quarter = warp & 3;     // TMEM lane quarter
         const int et = ew * 32 + lane;    // buffer column (0..255)
         const int row = quarter * 32 + lane;
         const int k = a.k;
-        const int kp = (k + 1) >> 1;      // union bound: ceil(k/2) per column group
+        constexpr uint32_t PLANE = CAP * EPI_THREADS * 16;  // bytes between the two value planes
+        const uint32_t sA0 = sm100::smem_u32(BA0) + static_cast<uint32_t>(et) * 16;
+        const uint32_t sI = sm100::smem_u32(BI) + static_cast<uint32_t>(et) * 4;
 
         RegList<KR> L;
         L.reset();
-        int cur_qt = -1;
-        int nb = 0;        // buffered candidates
+        int cur_p = -1, qt = 0;
+        int nb = 0;        // buffered candidate groups
         float T = kInf;    // own bound: thresh(k-th smallest A of this list)
-        float Tf = kInf;   // filter bound: min(T, other group's, other CTAs')
+        float Tf = kInf;   // filter bound: min(T, other CTAs' bounds for this query)
         unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
         Consts qc{};
         int64_t q = 0;
         int64_t t = 0;
-        uint64_t tagT = 0, tagP = 0;     // segment tags of the smem bound exchange
-        unsigned long long st_slow = 0, st_hits = 0, st_drains = 0, st_steps = 0;
+        unsigned long long st_pushed = 0, st_ins = 0, st_drains = 0, st_rounds = 0;
+        long long st_cyc_drain = 0, st_cyc_wait = 0;
+        const long long st_cyc0 = clock64();
 
-        // Insert every buffered candidate still under the bound, then refresh
-        // the bound from (1) this list, (2) the other column group's list of
-        // the same query (smem, tagged by segment), (3) the union of both
-        // groups' ceil(k/2)-th values, (4) other CTAs' parts of the query
-        // (global atomicMin, read one drain late so the load latency hides).
+        // Insert every buffered value still under the bound (one hit per lane
+        // per round), then refresh the bound from this list and from the other
+        // CTAs' lists of the same query (global atomicMin, read one drain late
+        // so the load latency hides).
 #define KNN_DRAIN()                                                                              \
     do {                                                                                         \
-        const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
-        if (a.stats) { ++st_drains; st_steps += mx_; st_slow += nb; }                            \
-        _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
-            if (j_ < nb) {                                                                       \
-                const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et];   \
-                const int c_ = BI[j_ * EPI_THREADS + et];                                        \
-                const float w_[8] = {p_.x, p_.y, p_.z, p_.w, q_.x, q_.y, q_.z, q_.w};            \
-                unsigned m_ = 0;                                                                 \
-                _Pragma("unroll") for (int e_ = 0; e_ < 8; ++e_) m_ |= (w_[e_] < Tf ? 1u : 0u) << e_; \
-                while (m_) { /* this lane's hits only: the warp runs max-popc rounds */          \
+        const long long c0_ = a.stats ? clock64() : 0;                                           \
+        if (a.stats) { ++st_drains; st_pushed += nb; }                                           \
+        {                                                                                        \
+            int j_ = 0, c_ = 0;                                                                  \
+            unsigned m_ = 0;                                                                     \
+            float w_[8];                                                                         \
+            while (true) {                                                                       \
+                while (m_ == 0 && j_ < nb) {                                                     \
+                    const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et]; \
+                    c_ = BI[j_ * EPI_THREADS + et];                                              \
+                    w_[0] = p_.x; w_[1] = p_.y; w_[2] = p_.z; w_[3] = p_.w;                      \
+                    w_[4] = q_.x; w_[5] = q_.y; w_[6] = q_.z; w_[7] = q_.w;                      \
+                    _Pragma("unroll") for (int e_ = 0; e_ < 8; ++e_)                             \
+                        m_ |= (w_[e_] < Tf ? 1u : 0u) << e_;                                     \
+                    ++j_;                                                                        \
+                }                                                                                \
+                if (!__any_sync(0xffffffffu, m_ != 0)) break;                                    \
+                if (a.stats) ++st_rounds;                                                        \
+                if (m_) {                                                                        \
                     const int e_ = __ffs(m_) - 1;                                                \
                     m_ &= m_ - 1;                                                                \
                     L.insert(sel8(w_, e_), c_ + e_);                                             \
+                    if (a.stats) ++st_ins;                                                       \
                 }                                                                                \
             }                                                                                    \
         }                                                                                        \
         nb = 0;                                                                                  \
         if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
         float tf_ = fminf(T, dec_or_inf(tg_pref));                                               \
-        if (T < kInf) {                                                                          \
-            atomicMin(a.tglob + q, enc(T));                                                      \
-            atomicMin(reinterpret_cast<unsigned long long*>(sT + row),                           \
-                      static_cast<unsigned long long>(tagT | enc(T)));                           \
-        }                                                                                        \
+        if (T < kInf) atomicMin(a.tglob + q, enc(T));                                            \
         tg_pref = __ldcg(a.tglob + q);                                                           \
-        const uint64_t so_ = sT[row];                                                            \
-        if ((so_ & 0xffffffff00000000ull) == tagT) tf_ = fminf(tf_, dec(static_cast<unsigned>(so_))); \
-        if (L.cnt >= kp) {                                                                       \
-            const float mine_ = L.kth(kp);                                                       \
-            sP[grp * TILE + row] = tagP | enc(mine_);                                            \
-            const uint64_t po_ = sP[(grp ^ 1) * TILE + row];                                     \
-            if ((po_ & 0xffffffff00000000ull) == tagP)                                           \
-                tf_ = fminf(tf_, thresh(fmaxf(mine_, dec(static_cast<unsigned>(po_))), qc));     \
-        }                                                                                        \
         Tf = tf_;                                                                                \
+        if (a.stats) st_cyc_drain += clock64() - c0_;                                            \
     } while (0)
 
-#define KNN_FLUSH(qt_)                                                                           \
+#define KNN_FLUSH(p_)                                                                            \
     do {                                                                                         \
-        const int64_t u0_ = static_cast<int64_t>(qt_) * a.rtiles;                                \
-        const int slot_ = cta - first_cta_of(u0_, a.U, a.G);                                    \
-        const int64_t part_ = (static_cast<int64_t>(qt_) * a.S_max + slot_) * 2 + grp;           \
+        const int64_t u0_ = static_cast<int64_t>(p_) * a.rtiles;                                 \
+        const int slot_ = cta - first_cta_of(u0_, a.U, a.G);                                     \
+        const int64_t part_ = static_cast<int64_t>(2 * (p_) + grp) * a.S_max + slot_;            \
         float* pa_ = a.part_A + part_ * a.Kq * TILE;                                             \
         int* pi_ = a.part_I + part_ * a.Kq * TILE;                                               \
         _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_) {                                      \
@@ -564,24 +600,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float* w_ = vv + 8 * i_;                                                       \
             const float gm_ = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]),   \
                                          w_[6]), w_[7]);                                         \
-            if (gm_ < Tf) {                                                                      \
-                BA0[nb * EPI_THREADS + et] = make_float4(w_[0], w_[1], w_[2], w_[3]);            \
-                BA1[nb * EPI_THREADS + et] = make_float4(w_[4], w_[5], w_[6], w_[7]);            \
-                BI[nb * EPI_THREADS + et] = (colb) + 8 * i_;                                     \
-                ++nb;                                                                            \
-            }                                                                                    \
+            const uint32_t o_ = static_cast<uint32_t>(nb) * (EPI_THREADS * 16);                  \
+            push_group(gm_, Tf, sA0 + o_, sA0 + PLANE + o_, sI + (o_ >> 2), w_, (colb) + 8 * i_); \
+            nb += gm_ < Tf ? 1 : 0;                                                              \
         }                                                                                        \
     } while (0)
 
-        int qt = static_cast<int>(u_begin / a.rtiles);
+        int p = static_cast<int>(u_begin / a.rtiles);
         int rt = static_cast<int>(u_begin % a.rtiles);
         for (int64_t u = u_begin; u < u_end; ++u, ++t) {
-            if (qt != cur_qt) {
-                if (cur_qt >= 0) {
+            if (p != cur_p) {
+                if (cur_p >= 0) {
                     KNN_DRAIN();
-                    KNN_FLUSH(cur_qt);
+                    KNN_FLUSH(cur_p);
                 }
-                cur_qt = qt;
+                cur_p = p;
+                qt = 2 * p + grp;
                 q = static_cast<int64_t>(qt) * TILE + row;
                 qc = load_consts(a, q);
                 L.reset();
@@ -589,77 +623,85 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tg_pref = __ldcg(a.tglob + q);
                 Tf = dec_or_inf(tg_pref);
                 nb = 0;
-                tagT = static_cast<uint64_t>(0x7fffffffu - static_cast<unsigned>(qt)) << 32;
-                tagP = static_cast<uint64_t>(qt) << 32;
             }
-            const int b = static_cast<int>(t % NBUF);
-            sm100::mbar_wait(tfull + b, static_cast<uint32_t>((t / NBUF) & 1));
+            const int b = static_cast<int>(t & 1);
+            const long long cw_ = a.stats ? clock64() : 0;
+            sm100::mbar_wait(tfull + 2 * grp + b, static_cast<uint32_t>((t >> 1) & 1));
+            if (a.stats) st_cyc_wait += clock64() - cw_;
             sm100::tc_fence_after();
             const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                   static_cast<uint32_t>(b * TILE + grp * 64);
-            const int col_base = rt * TILE + grp * 64;
+                                   static_cast<uint32_t>((2 * grp + b) * TILE);
+            const int col_base = rt * TILE;
             if (a.mode == 2) {
                 sm100::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + b);
+                if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
             } else {
-                uint32_t r0[32], r1[32];
-                sm100::tmem_ld_32x32b_x32(taddr, r0);
-                sm100::tmem_ld_32x32b_x32(taddr + 32, r1);
-                sm100::tmem_ld_wait();
-                sm100::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + b);  // registers hold the tile now
-                float v0[32], v1[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v0[j] = __uint_as_float(r0[j]);
-                    v1[j] = __uint_as_float(r1[j]);
-                }
-                if (!a.fold) {
-                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 w = __ldg(nr + j), w2 = __ldg(nr + 8 + j);
-                        v0[4 * j] += w.x;
-                        v0[4 * j + 1] += w.y;
-                        v0[4 * j + 2] += w.z;
-                        v0[4 * j + 3] += w.w;
-                        v1[4 * j] += w2.x;
-                        v1[4 * j + 1] += w2.y;
-                        v1[4 * j + 2] += w2.z;
-                        v1[4 * j + 3] += w2.w;
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {  // two 64-column halves (register budget)
+                    uint32_t r0[32], r1[32];
+                    sm100::tmem_ld_32x32b_x32(taddr + h * 64, r0);
+                    sm100::tmem_ld_32x32b_x32(taddr + h * 64 + 32, r1);
+                    sm100::tmem_ld_wait();
+                    if (h == 1) {  // registers hold the whole tile: release the buffer
+                        sm100::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
                     }
-                }
-                if (a.mode == 1) {
-                    float acc = kInf;
+                    float v0[32], v1[32];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 2) acc = min3(acc, v0[j], v1[j + 1]);
-                    if (acc == -1.f) a.sink[0] = acc;
-                } else {
-                    KNN_SCAN_CHUNK(v0, col_base);
-                    KNN_SCAN_CHUNK(v1, col_base + 32);
+                    for (int j = 0; j < 32; ++j) {
+                        v0[j] = __uint_as_float(r0[j]);
+                        v1[j] = __uint_as_float(r1[j]);
+                    }
+                    const int cb = col_base + h * 64;
+                    if (!a.fold) {
+                        const float4* nr = reinterpret_cast<const float4*>(a.rnorm + cb);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 w0 = __ldg(nr + j), w1 = __ldg(nr + 8 + j);
+                            v0[4 * j] += w0.x;
+                            v0[4 * j + 1] += w0.y;
+                            v0[4 * j + 2] += w0.z;
+                            v0[4 * j + 3] += w0.w;
+                            v1[4 * j] += w1.x;
+                            v1[4 * j + 1] += w1.y;
+                            v1[4 * j + 2] += w1.z;
+                            v1[4 * j + 3] += w1.w;
+                        }
+                    }
+                    if (a.mode == 1) {
+                        float acc = kInf;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) acc = min3(acc, v0[j], v1[j]);
+                        if (acc == -1.f) a.sink[0] = acc;
+                    } else {
+                        KNN_SCAN_CHUNK(v0, cb);
+                        KNN_SCAN_CHUNK(v1, cb + 32);
+                    }
                 }
             }
             if (++rt == a.rtiles) {
                 rt = 0;
-                ++qt;
+                ++p;
             }
         }
-        if (cur_qt >= 0) {
+        if (cur_p >= 0) {
             KNN_DRAIN();
-            KNN_FLUSH(cur_qt);
+            KNN_FLUSH(cur_p);
         }
         if (a.stats) {
-            st_hits = 0;
-            const unsigned long long w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(L.cnt));
-            const unsigned long long pushed = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_slow));
+            const unsigned long long pushed = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_pushed));
+            const unsigned long long ins = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_ins));
             if (lane == 0) {
                 atomicAdd(a.stats + 0, pushed);
                 atomicAdd(a.stats + 1, st_drains);
-                atomicAdd(a.stats + 2, st_steps);
-                atomicAdd(a.stats + 3, w + st_hits);
+                atomicAdd(a.stats + 2, st_rounds);
+                atomicAdd(a.stats + 3, ins);
                 atomicAdd(a.stats + 4, static_cast<unsigned long long>(t));
+                atomicAdd(a.stats + 5, static_cast<unsigned long long>(st_cyc_drain));
+                atomicAdd(a.stats + 6, static_cast<unsigned long long>(st_cyc_wait));
+                atomicAdd(a.stats + 7, static_cast<unsigned long long>(clock64() - st_cyc0));
             }
         }
 #undef KNN_SCAN_CHUNK
@@ -701,7 +743,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     if (q >= a.n) return;
     const int k = a.k;
     const int Kq = a.Kq;
-    const int parts = a.S_max * 2;  // <= 32 (checked on the host)
+    const int parts = a.S_max;  // <= 32 (checked on the host)
     const int span = parts * Kq;
     // per-warp staging: candidate A / index of every partial list, exact list
     float* sA = reinterpret_cast<float*>(smem_raw) + warp * span;
@@ -885,11 +927,11 @@ Layout layout_for(int d, int k) {
         ncol = L.d16;
     }
     const int kb_fold = (kfold + 63) / 64;
-    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 36 + 3 * TILE * 8;
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 36;
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
     auto stages_for = [&](int KB) {
         const size_t per = static_cast<size_t>(KB) * 16384;
-        const long avail = static_cast<long>(SMEM_LIMIT) - static_cast<long>(fixed + per);
+        const long avail = static_cast<long>(SMEM_LIMIT) - static_cast<long>(fixed + 2 * per);
         return avail > 0 ? static_cast<int>(avail / static_cast<long>(per)) : 0;
     };
     if (kb_fold == kb_plain || stages_for(kb_fold) >= 3) {
@@ -904,7 +946,7 @@ Layout layout_for(int d, int k) {
         L.norm_col = -1;
     }
     L.stages = std::min(stages_for(L.KB), 6);
-    L.smem = fixed + static_cast<size_t>(L.KB) * 16384 * (1 + L.stages);
+    L.smem = fixed + static_cast<size_t>(L.KB) * 16384 * (2 + L.stages);
     return L;
 }
 
@@ -920,23 +962,24 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
                      float* d_out, int64_t* d_idx) {
     const Layout L = layout_for(d, k);
-    const int qtiles = static_cast<int>((n + TILE - 1) / TILE);
+    const int pairs = static_cast<int>((n + 2 * TILE - 1) / (2 * TILE));
+    const int qtiles = 2 * pairs;  // the last tile of the last pair may be all padding
     const int rtiles = static_cast<int>((m + TILE - 1) / TILE);
     const int64_t n_pad = static_cast<int64_t>(qtiles) * TILE;
     const int64_t m_pad = static_cast<int64_t>(rtiles) * TILE;
-    const int64_t U = static_cast<int64_t>(qtiles) * rtiles;
-    // at most ~14 CTAs share a query tile, so a query has <= 32 partial lists
+    const int64_t U = static_cast<int64_t>(pairs) * rtiles;
+    // at most ~29 CTAs share a query-tile pair, so a query has <= 32 partial lists
     const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
-                                                     static_cast<int64_t>(qtiles) * 14));
+                                                     static_cast<int64_t>(pairs) * 29));
     // partial-list slots per query tile under the stream-K split
     int S_max = 1;
-    for (int qt = 0; qt < qtiles; ++qt) {
-        const int64_t u0 = static_cast<int64_t>(qt) * rtiles, u1 = u0 + rtiles - 1;
+    for (int pp = 0; pp < pairs; ++pp) {
+        const int64_t u0 = static_cast<int64_t>(pp) * rtiles, u1 = u0 + rtiles - 1;
         const int c0 = static_cast<int>((u0 * G) / U), c1 = static_cast<int>((u1 * G) / U);
         S_max = std::max(S_max, c1 - c0 + 3);  // +2 slack for floor rounding at the ends
     }
-    if (S_max > 16) throw CudaError("tensor path: too many partial lists per query tile");
-    const int64_t parts = static_cast<int64_t>(qtiles) * S_max * 2;
+    if (S_max > 32) throw CudaError("tensor path: too many partial lists per query tile");
+    const int64_t parts = static_cast<int64_t>(qtiles) * S_max;
 
     Sizer sz;
     sz.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -951,7 +994,6 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<float>(static_cast<size_t>(parts) * TILE);
     sz.take<int>(static_cast<size_t>(n) + 1);
     sz.take<unsigned>(static_cast<size_t>(n_pad));
-    sz.take<float>(static_cast<size_t>(n_pad) * 2 * S_max);
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -966,7 +1008,6 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     float* part_ev = cv.take<float>(static_cast<size_t>(parts) * TILE);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
-    float* pub = cv.take<float>(static_cast<size_t>(n_pad) * 2 * S_max);
     unsigned* gmax = mnmx + 2 * d;
     float* scale = mu + d;
 
@@ -976,8 +1017,6 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
-    // 0x7f7f7f7f = 3.4e38: "not yet published"
-    KNN_CUDA_CHECK(cudaMemsetAsync(pub, 0x7f, sizeof(float) * n_pad * 2 * S_max, stream));
     {
         ProfileScope ps(stream, "prep_range_kernel");
         range_kernel<<<static_cast<unsigned>((m + 63) / 64), 128, 0, stream>>>(dR, m, d, mnmx,
@@ -1025,6 +1064,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.n = n;
     fa.m = m;
     fa.qtiles = qtiles;
+    fa.pairs = pairs;
     fa.rtiles = rtiles;
     fa.U = U;
     fa.G = G;
@@ -1044,8 +1084,6 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.rnorm = rnorm;
     fa.gmax = gmax;
     fa.tglob = tglob;
-    fa.pub = pub;
-    fa.pmax = 2 * S_max;
     fa.part_A = part_A;
     fa.part_I = part_I;
     fa.part_cnt = part_cnt;
@@ -1082,10 +1120,10 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         KNN_CUDA_CHECK(cudaFree(fa.stats));
         const double warps = static_cast<double>(G) * EPI_WARPS;
         std::fprintf(stderr,
-                     "[filter stats] per warp: tiles %.1f groups-pushed/lane %.1f drains %.1f insert-steps "
-                     "%.1f | kept/list %.2f\n",
+                     "[filter stats] per warp: tiles %.1f groups-pushed/lane %.1f drains %.1f insert-rounds "
+                     "%.1f | inserts/lane %.2f | kcycles/warp: drain %.1f tfull-wait %.1f total %.1f\n",
                      h[4] / warps, h[0] / (warps * 32.0), h[1] / warps, h[2] / warps,
-                     h[3] / (warps * 32.0));
+                     h[3] / (warps * 32.0), h[5] / warps / 1e3, h[6] / warps / 1e3, h[7] / warps / 1e3);
     }
 
     // 3. exact re-rank
@@ -1106,7 +1144,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ra.fb_count = fb;
     ra.fb_list = fb + 1;
     const size_t rr_smem =
-        static_cast<size_t>(RR_WARPS) * (2 * 4 * S_max * 2 * L.Kq + static_cast<size_t>(k) * 12) + 16;
+        static_cast<size_t>(RR_WARPS) * (2 * 4 * S_max * L.Kq + static_cast<size_t>(k) * 12) + 16;
     {
         ProfileScope ps(stream, "rerank_kernel");
         rerank_kernel<<<static_cast<unsigned>((n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, rr_smem,
