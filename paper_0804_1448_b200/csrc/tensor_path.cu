@@ -54,7 +54,8 @@ constexpr int EPI_WARPS = 8;       // two groups of four (one warp per TMEM lane
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
 constexpr int NBUF = 4;            // TMEM accumulator buffers (4 x 128 columns = 512)
-constexpr int KEXTRA = 0;          // candidate list K' >= k + KEXTRA
+constexpr int KEXTRA = 0;          // bound list K' >= k + KEXTRA
+constexpr int kLogGroups = 256;    // logged candidate groups per (query, CTA part)
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
 
@@ -231,10 +232,12 @@ struct FilterArgs {
     const float* rnorm;    // no-fold norms
     const unsigned* gmax;
     unsigned* tglob;       // [n_pad] shared running threshold (ordered-uint, atomicMin)
-    float* part_A;         // [parts][Kq][128]
-    int* part_I;
-    int* part_cnt;         // [parts][128]
-    float* part_ev;        // [parts][128]
+    float* part_A;         // [parts][Kq][128] final bound list (keys) of each part
+    int* part_cnt;         // [parts][128] entries in part_A
+    int* log_n;            // [parts][128] groups logged (may exceed CG: overflow)
+    float4* log_v;         // [parts][128][CG][2] the 8 A values of each logged group
+    int* log_c;            // [parts][128][CG] first reference index of each logged group
+    int CG;                // log capacity (groups) per (part, query)
     int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 1 ld+min, 2 no epilogue work
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
@@ -266,18 +269,6 @@ __device__ __forceinline__ Consts load_consts(const FilterArgs& a, int64_t q) {
     return c;
 }
 
-// w[e] for a runtime e in [0, 8), as an opaque select chain (a plain dynamic
-// index would demote w to local memory)
-__device__ __forceinline__ float sel8(const float (&w)[8], int e) {
-    float x = w[0];
-#pragma unroll
-    for (int s = 1; s < 8; ++s)
-        asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\tselp.f32 %0, %1, %0, p;\n\t}"
-            : "+f"(x)
-            : "f"(w[s]), "r"(e), "r"(s));
-    return x;
-}
-
 __device__ __forceinline__ float min3(float x, float y, float z) {
     float w;
     asm("min.f32 %0, %1, %2, %3;" : "=f"(w) : "f"(x), "f"(y), "f"(z));
@@ -289,13 +280,13 @@ constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow, warpgrou
 constexpr int CTRL_REGS = 40;
 
 // Predicated append of one 8-value group to a lane's smem candidate buffer:
-// stores happen iff gm < tf (inline PTX so the compiler cannot turn the
+// stores happen iff gm <= tf (inline PTX so the compiler cannot turn the
 // predicate into a branch).  a0/a1: the slot's two float4 plane addresses,
 // ai: its column-base address (shared window).
 __device__ __forceinline__ void push_group(float gm, float tf, uint32_t a0, uint32_t a1, uint32_t ai,
                                            const float* w, int col) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %0, %1;\n\t"
+        "{\n\t.reg .pred p;\n\tsetp.le.f32 p, %0, %1;\n\t"
         "@p st.shared.v4.f32 [%2], {%5, %6, %7, %8};\n\t"
         "@p st.shared.v4.f32 [%3], {%9, %10, %11, %12};\n\t"
         "@p st.shared.b32 [%4], %13;\n\t}" ::"f"(gm),
@@ -304,46 +295,26 @@ __device__ __forceinline__ void push_group(float gm, float tf, uint32_t a0, uint
         : "memory");
 }
 
-// (a < b) ? if_lt : if_ge as one setp + selp (opaque: never a branch)
-__device__ __forceinline__ int sel_lt(float a, float b, int if_lt, int if_ge) {
-    int r;
-    asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tselp.b32 %0, %3, %4, p;\n\t}"
-        : "=r"(r)
-        : "f"(a), "f"(b), "r"(if_lt), "r"(if_ge));
-    return r;
-}
-
+// The KR smallest group minima seen by this (query, CTA part), sorted
+// ascending, keys only: the list exists to bound A_(k) (any k distinct
+// references with A <= v prove A_(k) <= v); candidate identities live in the
+// global group log, not here.
 template <int KR>
 struct RegList {
     float key[KR];
-    int idx[KR];
     int cnt;
-    float evict;  // smallest A ever dropped for capacity (certificate input)
 
     __device__ __forceinline__ void reset() {
 #pragma unroll
-        for (int s = 0; s < KR; ++s) {
-            key[s] = kInf;
-            idx[s] = 0x7fffffff;
-        }
+        for (int s = 0; s < KR; ++s) key[s] = kInf;
         cnt = 0;
-        evict = kInf;
     }
-    // branch-free compare-swap insertion chain (no dynamic register indexing)
-    // Insert by rank, branch-free: slot s becomes max(key[s-1], min(x, key[s]))
-    // (= key[s-1] if x sorts before it, x if it lands here, else unchanged) and
-    // the index follows with two predicated selects.  Every slot depends only
-    // on x and the old list, so there is no serial chain; the selects are
-    // inline PTX because the compiler otherwise turns them into per-slot
-    // branches (ties: x goes after equal keys).
-    __device__ __forceinline__ void insert(float x, int xi) {
-        evict = fminf(evict, fmaxf(x, key[KR - 1]));  // +inf while the list is not full
+    // Branch-free insert by rank: slot s becomes max(key[s-1], min(x, key[s]))
+    // (= key[s-1] if x sorts before it, x if it lands here, else unchanged).
+    // Every slot depends only on x and the old list: no serial chain.
+    __device__ __forceinline__ void insert(float x) {
 #pragma unroll
-        for (int s = KR - 1; s > 0; --s) {
-            idx[s] = sel_lt(x, key[s - 1], idx[s - 1], sel_lt(x, key[s], xi, idx[s]));
-            key[s] = fmaxf(key[s - 1], fminf(x, key[s]));
-        }
-        idx[0] = sel_lt(x, key[0], xi, idx[0]);
+        for (int s = KR - 1; s > 0; --s) key[s] = fmaxf(key[s - 1], fminf(x, key[s]));
         key[0] = fminf(x, key[0]);
         cnt = min(cnt + 1, KR);
     }
@@ -525,38 +496,40 @@ __global__ void __launch_bounds__(THREADS, 1)
         Consts qc{};
         int64_t q = 0;
         int64_t t = 0;
+        int64_t part = 0;
+        float4* lv = nullptr;  // this (query, part)'s group log
+        int* lc = nullptr;
+        int ln = 0;            // groups logged so far (may exceed CG: overflow)
         unsigned long long st_pushed = 0, st_ins = 0, st_drains = 0, st_rounds = 0;
         long long st_cyc_drain = 0, st_cyc_wait = 0;
         const long long st_cyc0 = clock64();
 
-        // Insert every buffered value still under the bound (one hit per lane
-        // per round), then refresh the bound from this list and from the other
-        // CTAs' lists of the same query (global atomicMin, read one drain late
-        // so the load latency hides).
+        // Drain: one buffered group per lane per round.  A group whose minimum
+        // is still under the (possibly tightened) bound is inserted into the
+        // bound list by its minimum and appended whole to the query's global
+        // group log (the re-rank reads the candidates from there).  Then the
+        // bound is refreshed from this list and from the other CTAs' lists of
+        // the same query (global atomicMin, read one drain late so the load
+        // latency hides).
 #define KNN_DRAIN()                                                                              \
     do {                                                                                         \
         const long long c0_ = a.stats ? clock64() : 0;                                           \
         if (a.stats) { ++st_drains; st_pushed += nb; }                                           \
-        {                                                                                        \
-            int j_ = 0, c_ = 0;                                                                  \
-            unsigned m_ = 0;                                                                     \
-            float w_[8];                                                                         \
-            while (true) {                                                                       \
-                while (m_ == 0 && j_ < nb) {                                                     \
-                    const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et]; \
-                    c_ = BI[j_ * EPI_THREADS + et];                                              \
-                    w_[0] = p_.x; w_[1] = p_.y; w_[2] = p_.z; w_[3] = p_.w;                      \
-                    w_[4] = q_.x; w_[5] = q_.y; w_[6] = q_.z; w_[7] = q_.w;                      \
-                    _Pragma("unroll") for (int e_ = 0; e_ < 8; ++e_)                             \
-                        m_ |= (w_[e_] < Tf ? 1u : 0u) << e_;                                     \
-                    ++j_;                                                                        \
-                }                                                                                \
-                if (!__any_sync(0xffffffffu, m_ != 0)) break;                                    \
-                if (a.stats) ++st_rounds;                                                        \
-                if (m_) {                                                                        \
-                    const int e_ = __ffs(m_) - 1;                                                \
-                    m_ &= m_ - 1;                                                                \
-                    L.insert(sel8(w_, e_), c_ + e_);                                             \
+        const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
+        _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
+            if (a.stats) ++st_rounds;                                                            \
+            if (j_ < nb) {                                                                       \
+                const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et];   \
+                const int c_ = BI[j_ * EPI_THREADS + et];                                        \
+                const float g_ = fminf(min3(min3(p_.x, p_.y, p_.z), min3(p_.w, q_.x, q_.y), q_.z), q_.w); \
+                if (g_ <= Tf) {                                                                  \
+                    L.insert(g_);                                                                \
+                    if (ln < a.CG) {                                                             \
+                        lv[2 * ln] = p_;                                                         \
+                        lv[2 * ln + 1] = q_;                                                     \
+                        lc[ln] = c_;                                                             \
+                    }                                                                            \
+                    ++ln;                                                                        \
                     if (a.stats) ++st_ins;                                                       \
                 }                                                                                \
             }                                                                                    \
@@ -570,21 +543,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (a.stats) st_cyc_drain += clock64() - c0_;                                            \
     } while (0)
 
-#define KNN_FLUSH(p_)                                                                            \
+#define KNN_FLUSH()                                                                              \
     do {                                                                                         \
-        const int64_t u0_ = static_cast<int64_t>(p_) * a.rtiles;                                 \
-        const int slot_ = cta - first_cta_of(u0_, a.U, a.G);                                     \
-        const int64_t part_ = static_cast<int64_t>(2 * (p_) + grp) * a.S_max + slot_;            \
-        float* pa_ = a.part_A + part_ * a.Kq * TILE;                                             \
-        int* pi_ = a.part_I + part_ * a.Kq * TILE;                                               \
-        _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_) {                                      \
-            if (e_ < L.cnt) {                                                                    \
-                pa_[e_ * TILE + row] = L.key[e_];                                                \
-                pi_[e_ * TILE + row] = L.idx[e_];                                                \
-            }                                                                                    \
-        }                                                                                        \
-        a.part_cnt[part_ * TILE + row] = L.cnt;                                                  \
-        a.part_ev[part_ * TILE + row] = L.evict;                                                 \
+        float* pa_ = a.part_A + part * a.Kq * TILE;                                              \
+        _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_)                                        \
+            if (e_ < L.cnt) pa_[e_ * TILE + row] = L.key[e_];                                    \
+        a.part_cnt[part * TILE + row] = L.cnt;                                                   \
+        a.log_n[part * TILE + row] = ln;                                                         \
     } while (0)
 
         // One 32-column chunk, branch-free: the minimum of each 8-column group
@@ -602,7 +567,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                          w_[6]), w_[7]);                                         \
             const uint32_t o_ = static_cast<uint32_t>(nb) * (EPI_THREADS * 16);                  \
             push_group(gm_, Tf, sA0 + o_, sA0 + PLANE + o_, sI + (o_ >> 2), w_, (colb) + 8 * i_); \
-            nb += gm_ < Tf ? 1 : 0;                                                              \
+            nb += gm_ <= Tf ? 1 : 0;                                                             \
         }                                                                                        \
     } while (0)
 
@@ -612,11 +577,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (p != cur_p) {
                 if (cur_p >= 0) {
                     KNN_DRAIN();
-                    KNN_FLUSH(cur_p);
+                    KNN_FLUSH();
                 }
                 cur_p = p;
                 qt = 2 * p + grp;
                 q = static_cast<int64_t>(qt) * TILE + row;
+                {
+                    const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
+                    part = static_cast<int64_t>(qt) * a.S_max + slot;
+                    const int64_t lq = (part * TILE + row) * a.CG;
+                    lv = a.log_v + 2 * lq;
+                    lc = a.log_c + lq;
+                    ln = 0;
+                }
                 qc = load_consts(a, q);
                 L.reset();
                 T = kInf;
@@ -637,48 +610,46 @@ __global__ void __launch_bounds__(THREADS, 1)
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
             } else {
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {  // two 64-column halves (register budget)
-                    uint32_t r0[32], r1[32];
-                    sm100::tmem_ld_32x32b_x32(taddr + h * 64, r0);
-                    sm100::tmem_ld_32x32b_x32(taddr + h * 64 + 32, r1);
-                    sm100::tmem_ld_wait();
-                    if (h == 1) {  // registers hold the whole tile: release the buffer
-                        sm100::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
-                    }
-                    float v0[32], v1[32];
+                uint32_t r0[32], r1[32], r2[32], r3[32];
+                sm100::tmem_ld_32x32b_x32(taddr, r0);
+                sm100::tmem_ld_32x32b_x32(taddr + 32, r1);
+                sm100::tmem_ld_32x32b_x32(taddr + 64, r2);
+                sm100::tmem_ld_32x32b_x32(taddr + 96, r3);
+                sm100::tmem_ld_wait();
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);  // registers hold the tile
+                float v[4][32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        v0[j] = __uint_as_float(r0[j]);
-                        v1[j] = __uint_as_float(r1[j]);
-                    }
-                    const int cb = col_base + h * 64;
-                    if (!a.fold) {
-                        const float4* nr = reinterpret_cast<const float4*>(a.rnorm + cb);
+                for (int j = 0; j < 32; ++j) {
+                    v[0][j] = __uint_as_float(r0[j]);
+                    v[1][j] = __uint_as_float(r1[j]);
+                    v[2][j] = __uint_as_float(r2[j]);
+                    v[3][j] = __uint_as_float(r3[j]);
+                }
+                if (!a.fold) {
+                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            const float4 w0 = __ldg(nr + j), w1 = __ldg(nr + 8 + j);
-                            v0[4 * j] += w0.x;
-                            v0[4 * j + 1] += w0.y;
-                            v0[4 * j + 2] += w0.z;
-                            v0[4 * j + 3] += w0.w;
-                            v1[4 * j] += w1.x;
-                            v1[4 * j + 1] += w1.y;
-                            v1[4 * j + 2] += w1.z;
-                            v1[4 * j + 3] += w1.w;
+                            const float4 w = __ldg(nr + 8 * c + j);
+                            v[c][4 * j] += w.x;
+                            v[c][4 * j + 1] += w.y;
+                            v[c][4 * j + 2] += w.z;
+                            v[c][4 * j + 3] += w.w;
                         }
-                    }
-                    if (a.mode == 1) {
-                        float acc = kInf;
+                }
+                if (a.mode == 1) {
+                    float acc = kInf;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) acc = min3(acc, v0[j], v1[j]);
-                        if (acc == -1.f) a.sink[0] = acc;
-                    } else {
-                        KNN_SCAN_CHUNK(v0, cb);
-                        KNN_SCAN_CHUNK(v1, cb + 32);
-                    }
+                    for (int j = 0; j < 32; ++j) acc = min3(acc, min3(v[0][j], v[1][j], v[2][j]), v[3][j]);
+                    if (acc == -1.f) a.sink[0] = acc;
+                } else {
+                    KNN_SCAN_CHUNK(v[0], col_base);
+                    KNN_SCAN_CHUNK(v[1], col_base + 32);
+                    KNN_SCAN_CHUNK(v[2], col_base + 64);
+                    KNN_SCAN_CHUNK(v[3], col_base + 96);
                 }
             }
             if (++rt == a.rtiles) {
@@ -688,7 +659,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (cur_p >= 0) {
             KNN_DRAIN();
-            KNN_FLUSH(cur_p);
+            KNN_FLUSH();
         }
         if (a.stats) {
             const unsigned long long pushed = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_pushed));
@@ -745,41 +716,33 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     const int Kq = a.Kq;
     const int parts = a.S_max;  // <= 32 (checked on the host)
     const int span = parts * Kq;
-    // per-warp staging: candidate A / index of every partial list, exact list
+    // per-warp staging: every part's bound list, then the exact list
     float* sA = reinterpret_cast<float*>(smem_raw) + warp * span;
-    int* sI = reinterpret_cast<int*>(reinterpret_cast<float*>(smem_raw) + RR_WARPS * span) +
-              warp * span;
-    float* fk = reinterpret_cast<float*>(smem_raw) + 2 * RR_WARPS * span + warp * k;
+    float* fk = reinterpret_cast<float*>(smem_raw) + RR_WARPS * span + warp * k;
     int64_t* fi = reinterpret_cast<int64_t*>(reinterpret_cast<float*>(smem_raw) +
-                                             2 * RR_WARPS * span + RR_WARPS * k) +
-                  warp * k;  // byte offset 16*(2*span + k): 8-B aligned
+                                             RR_WARPS * span + RR_WARPS * k) +
+                  warp * k;  // byte offset 4*(4*span + 4*k): 8-B aligned
 
     const int qt = static_cast<int>(q / TILE);
     const int row = static_cast<int>(q % TILE);
     const int64_t p0 = static_cast<int64_t>(qt) * parts;
 
-    int cnt = 0;
-    float ev = kInf;
+    int cnt = 0, nlog = 0;
     if (lane < parts) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
-        ev = a.f.part_ev[(p0 + lane) * TILE + row];
+        nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
-    // 0. stage every list (independent loads, one round trip)
+    // 0. stage every bound list (independent loads, one round trip)
     for (int x = lane; x < span; x += 32) {
         const int p = x / Kq, e = x - p * Kq;
-        float va = kInf;
-        int vi = 0x7fffffff;
         const int64_t part = p0 + p;
-        if (e < a.f.part_cnt[part * TILE + row]) {
-            va = a.f.part_A[(part * Kq + e) * TILE + row];
-            vi = a.f.part_I[(part * Kq + e) * TILE + row];
-        }
-        sA[x] = va;
-        sI[x] = vi;
+        sA[x] = e < a.f.part_cnt[part * TILE + row] ? a.f.part_A[(part * Kq + e) * TILE + row]
+                                                     : kInf;
     }
     __syncwarp();
 
-    // 1. k-th smallest A over all lists: k-step tournament on the sorted list heads
+    // 1. k-th smallest group minimum over all lists (k distinct references):
+    //    k-step tournament on the sorted list heads
     int head = 0;
     float hv = (lane < parts && cnt > 0) ? sA[lane * Kq] : kInf;
     float ak = kInf;
@@ -804,8 +767,9 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     const Consts qc = load_consts(a.f, q);
     const float tau = thresh(ak, qc);
 
-    // 2. certificate: nothing within tau was ever dropped for capacity
-    const bool ok = __all_sync(0xffffffffu, cnt == 0 || ev > tau) && isfinite(tau);
+    // 2. certificate: every group that ever passed a filter bound (>= tau) is
+    //    in its part's log, i.e. no log overflowed
+    const bool ok = __all_sync(0xffffffffu, nlog <= a.f.CG) && isfinite(tau);
     if (!ok) {
         if (lane == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
@@ -851,22 +815,42 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         LF.offer<1>(ck, ci, lane);
         myj = -1;
     };
-    for (int x0 = 0; x0 < span; x0 += 32) {
-        const int x = x0 + lane;
-        const bool c = x < span && sA[x] <= tau;
-        const unsigned bal = __ballot_sync(0xffffffffu, c);
-        const int pos = taken + __popc(bal & ((1u << lane) - 1u));
-        const int j = c ? sI[x] : -1;
-        unsigned rem = bal;
-        while (rem) {
-            const int src = __ffs(rem) - 1;
-            rem &= rem - 1;
-            const int pj = __shfl_sync(0xffffffffu, j, src);
-            const int pp = __shfl_sync(0xffffffffu, pos, src);
-            if ((pp & 31) == lane) myj = pj;
-            if ((pp & 31) == 31) emit();  // 32 candidates assembled
+    // logged groups of every part: values <= tau are the candidates
+    for (int p = 0; p < parts; ++p) {
+        const int np = __shfl_sync(0xffffffffu, nlog, p);
+        const int64_t lq = ((p0 + p) * TILE + row) * a.f.CG;
+        for (int g0 = 0; g0 < np; g0 += 32) {
+            const int g = g0 + lane;
+            float w[8];
+            int c0 = 0;
+            if (g < np) {
+                const float4 u = a.f.log_v[2 * (lq + g)], v = a.f.log_v[2 * (lq + g) + 1];
+                w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+                w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
+                c0 = a.f.log_c[lq + g];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w[e] = kInf;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool c = w[e] <= tau;
+                const unsigned bal = __ballot_sync(0xffffffffu, c);
+                if (bal == 0u) continue;
+                const int pos = taken + __popc(bal & ((1u << lane) - 1u));
+                const int j = c ? c0 + e : -1;
+                unsigned rem = bal;
+                while (rem) {
+                    const int src = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    const int pj = __shfl_sync(0xffffffffu, j, src);
+                    const int pp = __shfl_sync(0xffffffffu, pos, src);
+                    if ((pp & 31) == lane) myj = pj;
+                    if ((pp & 31) == 31) emit();  // 32 candidates assembled
+                }
+                taken += __popc(bal);
+            }
         }
-        taken += __popc(bal);
     }
     if (taken & 31) emit();
     __syncwarp();
@@ -988,10 +972,12 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<float4>(static_cast<size_t>(n_pad));
     sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
     sz.take<float>(static_cast<size_t>(d) + 1);
+    const int CG = kLogGroups;
     sz.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
-    sz.take<int>(static_cast<size_t>(parts) * L.Kq * TILE);
     sz.take<int>(static_cast<size_t>(parts) * TILE);
-    sz.take<float>(static_cast<size_t>(parts) * TILE);
+    sz.take<int>(static_cast<size_t>(parts) * TILE);
+    sz.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
+    sz.take<int>(static_cast<size_t>(parts) * TILE * CG);
     sz.take<int>(static_cast<size_t>(n) + 1);
     sz.take<unsigned>(static_cast<size_t>(n_pad));
     ctx.arena.reserve(sz.used + 256);
@@ -1003,9 +989,10 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     unsigned* mnmx = cv.take<unsigned>(2 * static_cast<size_t>(d) + 2);
     float* mu = cv.take<float>(static_cast<size_t>(d) + 1);
     float* part_A = cv.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
-    int* part_I = cv.take<int>(static_cast<size_t>(parts) * L.Kq * TILE);
     int* part_cnt = cv.take<int>(static_cast<size_t>(parts) * TILE);
-    float* part_ev = cv.take<float>(static_cast<size_t>(parts) * TILE);
+    int* log_n = cv.take<int>(static_cast<size_t>(parts) * TILE);
+    float4* log_v = cv.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
+    int* log_c = cv.take<int>(static_cast<size_t>(parts) * TILE * CG);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
     unsigned* gmax = mnmx + 2 * d;
@@ -1015,6 +1002,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     KNN_CUDA_CHECK(cudaMemsetAsync(mnmx, 0xff, sizeof(unsigned) * d, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(mnmx + d, 0x00, sizeof(unsigned) * d, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(log_n, 0, sizeof(int) * parts * TILE, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
     {
@@ -1085,11 +1073,13 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.gmax = gmax;
     fa.tglob = tglob;
     fa.part_A = part_A;
-    fa.part_I = part_I;
     fa.part_cnt = part_cnt;
-    fa.part_ev = part_ev;
+    fa.log_n = log_n;
+    fa.log_v = log_v;
+    fa.log_c = log_c;
+    fa.CG = CG;
     if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
-    fa.sink = part_ev;
+    fa.sink = reinterpret_cast<float*>(log_n);
     const bool want_stats = std::getenv("KNN_B200_FILTER_STATS") != nullptr;
     if (want_stats) {
         KNN_CUDA_CHECK(cudaMallocAsync(&fa.stats, 8 * sizeof(unsigned long long), stream));
@@ -1121,7 +1111,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         const double warps = static_cast<double>(G) * EPI_WARPS;
         std::fprintf(stderr,
                      "[filter stats] per warp: tiles %.1f groups-pushed/lane %.1f drains %.1f insert-rounds "
-                     "%.1f | inserts/lane %.2f | kcycles/warp: drain %.1f tfull-wait %.1f total %.1f\n",
+                     "%.1f | logged-groups/lane %.2f | kcycles/warp: drain %.1f tfull-wait %.1f total %.1f\n",
                      h[4] / warps, h[0] / (warps * 32.0), h[1] / warps, h[2] / warps,
                      h[3] / (warps * 32.0), h[5] / warps / 1e3, h[6] / warps / 1e3, h[7] / warps / 1e3);
     }
@@ -1144,7 +1134,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ra.fb_count = fb;
     ra.fb_list = fb + 1;
     const size_t rr_smem =
-        static_cast<size_t>(RR_WARPS) * (2 * 4 * S_max * L.Kq + static_cast<size_t>(k) * 12) + 16;
+        static_cast<size_t>(RR_WARPS) * (4 * S_max * L.Kq + static_cast<size_t>(k) * 12) + 16;
     {
         ProfileScope ps(stream, "rerank_kernel");
         rerank_kernel<<<static_cast<unsigned>((n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, rr_smem,

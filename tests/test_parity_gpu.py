@@ -244,21 +244,29 @@ def test_large_d_and_odd_shapes(knn, oracle):
 
 def test_tensor_path_is_used_and_certified(knn, oracle):
     """Random data: every query certified by the tcgen05 candidate bound (no
-    exact-kernel fallback); duplicate-heavy data: certificate fails, fallback
-    recomputes, results still exact."""
+    exact-kernel fallback).  Duplicate-heavy data: the candidate-group log
+    holds every reference inside the bound, still certified and exact.  All
+    references identical: every group passes the bound, a log overflows, the
+    certificate fails and the exact kernel recomputes -- results still exact."""
     R = oracle.uniform_f32(20000, 96, 31)
     Q = oracle.uniform_f32(3000, 96, 32)
     t = knn.bf_knn(Q, R, 20, config=knn.BfConfig(path=knn.PATH_TENSOR))
     assert knn.last_fallback_count() == 0
     ri, rd = oracle.knn(Q[:300], R, 20)
     assert compare(t.index[:300], t.distance[:300], ri, rd, Q[:300], R, oracle=oracle).ok
-    # 40 copies of every point: > K' candidates inside the bound -> fallback
+    # 40 copies of every point: many exact ties inside the bound
     base = oracle.uniform_f32(100, 16, 33)
     Rd = np.repeat(base, 40, axis=0)
     Qd = oracle.uniform_f32(50, 16, 34)
     td = knn.bf_knn(Qd, Rd, 20, config=knn.BfConfig(path=knn.PATH_TENSOR))
-    assert knn.last_fallback_count() > 0
     te = knn.bf_knn(Qd, Rd, 20, config=knn.BfConfig(path=knn.PATH_EXACT))
     assert (td.index == te.index).all() and (td.distance == te.distance).all()
     ri, rd = oracle.knn(Qd, Rd, 20)
     assert compare(td.index, td.distance, ri, rd, Qd, Rd, oracle=oracle).ok
+    # one point repeated: every 8-reference group is a candidate -> log overflow
+    Rs = np.repeat(oracle.uniform_f32(1, 16, 35), 80000, axis=0)
+    ts = knn.bf_knn(Qd, Rs, 20, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() > 0
+    tse = knn.bf_knn(Qd, Rs, 20, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (ts.index == tse.index).all() and (ts.distance == tse.distance).all()
+    assert (ts.index == np.arange(20)[None, :]).all()
