@@ -102,20 +102,60 @@ __device__ __forceinline__ float dec_or_inf(unsigned u) {
     return fminf(kInf, dec(u));
 }
 
-// per-dimension min / max over the rows of X (both point sets)
-__global__ void range_kernel(const float* X, int64_t rows, int d, unsigned* mn, unsigned* mx) {
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
-    const int64_t r1 = min(rows, r0 + 64);
+// Per-dimension min / max over the rows of X (both point sets).  Grid-stride
+// over rows with a fixed column group per thread (VEC columns, 16-B loads when
+// d % 4 == 0), so loads are coalesced and independent; the block reduces in
+// shared memory and issues one global atomic per column.
+template <int VEC>
+__global__ void __launch_bounds__(256) range_kernel(const float* X, int64_t rows, int d, unsigned* mn,
+                                                    unsigned* mx) {
+    __shared__ unsigned smn[128], smx[128];
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        float lo = kInf, hi = -kInf;
-        for (int64_t r = r0; r < r1; ++r) {
-            const float v = __ldg(X + r * d + c);
-            lo = fminf(lo, v);
-            hi = fmaxf(hi, v);
+        smn[c] = 0xffffffffu;
+        smx[c] = 0u;
+    }
+    __syncthreads();
+    const int dq = d / VEC;                       // column groups per row
+    const int rpb = static_cast<int>(blockDim.x) / dq;  // rows per block step
+    const int t = threadIdx.x;
+    if (t < rpb * dq) {
+        const int cg = t % dq, rs = t / dq;
+        float lo[VEC], hi[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            lo[v] = kInf;
+            hi[v] = -kInf;
         }
-        if (r1 > r0) {
-            atomicMin(mn + c, enc(lo));
-            atomicMax(mx + c, enc(hi));
+        const int64_t step = static_cast<int64_t>(gridDim.x) * rpb;
+#pragma unroll 4
+        for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpb + rs; r < rows; r += step) {
+            if constexpr (VEC == 4) {
+                const float4 x4 = __ldg(reinterpret_cast<const float4*>(X + r * d) + cg);
+                const float x[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    lo[v] = fminf(lo[v], x[v]);
+                    hi[v] = fmaxf(hi[v], x[v]);
+                }
+            } else {
+                const float x = __ldg(X + r * d + cg);
+                lo[0] = fminf(lo[0], x);
+                hi[0] = fmaxf(hi[0], x);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            if (lo[v] <= hi[v]) {
+                atomicMin(smn + cg * VEC + v, enc(lo[v]));
+                atomicMax(smx + cg * VEC + v, enc(hi[v]));
+            }
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        if (smn[c] != 0xffffffffu) {
+            atomicMin(mn + c, smn[c]);
+            atomicMax(mx + c, smx[c]);
         }
     }
 }
@@ -154,43 +194,47 @@ __global__ void scale_kernel(const unsigned* mn, const unsigned* mx, int d, int 
 
 // warp per row: fp16 conversion, folded norm, rounding radius
 template <bool QUERY>
-__global__ void convert_kernel(PrepArgs a) {
+__global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
+    __shared__ float red[2][8];
     const int lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (row >= a.rows_pad) return;
+    const int wib = threadIdx.x >> 5;
     const float s = *a.scale;
-    const bool real = row < a.rows;
-    double h2 = 0.0, e2 = 0.0;
-    __half* out = a.Xh + row * a.Kp;
-    for (int c = lane; c < a.Kp; c += 32) {
-        __half h = __float2half_rn(0.f);
-        if (real && c < a.d) {
-            const float t = __fsub_rn(__ldg(a.X + row * a.d + c), a.mu[c]) * s;
-            h = __float2half_rn(t);
-            const double hv = static_cast<double>(__half2float(h));
-            // fp16 rounding + the fp32 subtraction's rounding (<= 2^-24 |t|, doubled)
-            const double err = fabs(hv - static_cast<double>(t)) + fabs(static_cast<double>(t)) * 0x1.0p-23;
-            h2 += hv * hv;
-            e2 += err * err;
-            if (QUERY) h = __float2half_rn(-2.f * __half2float(h));  // exact: power-of-two scale
+    // reference sets: running maxima of the rounding radius and of ||r~||,
+    // reduced per block (one global atomic per block, not per row)
+    float dmax = 0.f, nmax = 0.f;
+    const int64_t wstep = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib; row < a.rows_pad;
+         row += wstep) {
+        const bool real = row < a.rows;
+        double h2 = 0.0, e2 = 0.0;
+        __half* out = a.Xh + row * a.Kp;
+        for (int c = lane; c < a.Kp; c += 32) {
+            __half h = __float2half_rn(0.f);
+            if (real && c < a.d) {
+                const float t = __fsub_rn(__ldg(a.X + row * a.d + c), a.mu[c]) * s;
+                h = __float2half_rn(t);
+                const double hv = static_cast<double>(__half2float(h));
+                // fp16 rounding + the fp32 subtraction's rounding (<= 2^-24 |t|, doubled)
+                const double err = fabs(hv - static_cast<double>(t)) + fabs(static_cast<double>(t)) * 0x1.0p-23;
+                h2 += hv * hv;
+                e2 += err * err;
+                if (QUERY) h = __float2half_rn(-2.f * __half2float(h));  // exact: power-of-two scale
+            }
+            out[c] = h;
         }
-        out[c] = h;
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
-        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-    }
-    __syncwarp();
-    if (lane == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        }
         const float delta = static_cast<float>(sqrt(e2) * (1.0 + 0x1.0p-20)) * (1.f + 1e-6f);
         const float xn = static_cast<float>(sqrt(h2)) * (1.f + 1e-6f);
-        if (QUERY) {
-            if (a.norm_col >= 0)
-                for (int j = 0; j < 3; ++j) out[a.norm_col + j] = __float2half_rn(1.f);
-            a.qconst[row] = make_float4(static_cast<float>(h2), delta, xn, 0.f);
-        } else {
-            if (a.norm_col >= 0) {
+        if (lane == 0) {
+            if (QUERY) {
+                if (a.norm_col >= 0)
+                    for (int j = 0; j < 3; ++j) out[a.norm_col + j] = __float2half_rn(1.f);
+                a.qconst[row] = make_float4(static_cast<float>(h2), delta, xn, 0.f);
+            } else if (a.norm_col >= 0) {
                 if (real) {
                     const __half p1 = __double2half(h2);
                     const double r1 = h2 - static_cast<double>(__half2float(p1));
@@ -200,15 +244,31 @@ __global__ void convert_kernel(PrepArgs a) {
                     out[a.norm_col + 1] = p2;
                     out[a.norm_col + 2] = __double2half(r2);
                 } else {
-                    out[a.norm_col] = __float2half_rn(kInf);
+                    out[a.norm_col] = __float2half_rn(kInf);  // padding: A = +inf
                 }
             } else {
                 a.norm[row] = real ? static_cast<float>(h2) : kInf;
             }
-            if (real) {
-                atomicMax(a.gmax + 0, __float_as_uint(delta));
-                atomicMax(a.gmax + 1, __float_as_uint(xn));
+        }
+        if (!QUERY && real) {
+            dmax = fmaxf(dmax, delta);
+            nmax = fmaxf(nmax, xn);
+        }
+    }
+    if (!QUERY) {
+        if (lane == 0) {
+            red[0][wib] = dmax;
+            red[1][wib] = nmax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float dm = 0.f, nm = 0.f;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+                dm = fmaxf(dm, red[0][w]);
+                nm = fmaxf(nm, red[1][w]);
             }
+            atomicMax(a.gmax + 0, __float_as_uint(dm));  // non-negative floats order as uints
+            atomicMax(a.gmax + 1, __float_as_uint(nm));
         }
     }
 }
@@ -705,7 +765,19 @@ struct RerankArgs {
 };
 
 constexpr int RR_WARPS = 4;
+constexpr int RR_CAND = 128;  // exact candidates per query on the fast path (more: fallback)
 
+__host__ __device__ constexpr size_t rr_warp_bytes(int span, int k) {
+    return ((static_cast<size_t>(span) * 4 + RR_CAND * 8 + static_cast<size_t>(k) * 4 + 15) / 16) * 16 +
+           static_cast<size_t>(k) * 8;
+}
+
+// Warp per query.  (1) A_bound = k-th smallest of the union of the parts'
+// bound lists (rank counting over the compacted lists); tau = thresh(A_bound).
+// (2) Certificate: no part's group log overflowed, so every reference with
+// A <= tau is in a log (every filter bound was >= tau).  (3) Candidates =
+// logged values <= tau; their exact FP32 keys (key_step<kL2>, bitwise the
+// exact kernel's arithmetic); (4) exact top-k by (key, index) rank counting.
 __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -716,12 +788,13 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     const int Kq = a.Kq;
     const int parts = a.S_max;  // <= 32 (checked on the host)
     const int span = parts * Kq;
-    // per-warp staging: every part's bound list, then the exact list
-    float* sA = reinterpret_cast<float*>(smem_raw) + warp * span;
-    float* fk = reinterpret_cast<float*>(smem_raw) + RR_WARPS * span + warp * k;
-    int64_t* fi = reinterpret_cast<int64_t*>(reinterpret_cast<float*>(smem_raw) +
-                                             RR_WARPS * span + RR_WARPS * k) +
-                  warp * k;  // byte offset 4*(4*span + 4*k): 8-B aligned
+    unsigned char* wb = smem_raw + static_cast<size_t>(warp) * rr_warp_bytes(span, k);
+    float* sv = reinterpret_cast<float*>(wb);                 // [span] compacted bound lists
+    float* ck = sv + span;                                     // [RR_CAND] exact keys
+    int* ci = reinterpret_cast<int*>(ck + RR_CAND);            // [RR_CAND] reference indices
+    float* fk = reinterpret_cast<float*>(ci + RR_CAND);        // [k] result keys
+    int64_t* fi = reinterpret_cast<int64_t*>(
+        wb + ((static_cast<size_t>(span) * 4 + RR_CAND * 8 + static_cast<size_t>(k) * 4 + 15) / 16) * 16);
 
     const int qt = static_cast<int>(q / TILE);
     const int row = static_cast<int>(q % TILE);
@@ -732,44 +805,75 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
         nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
-    // 0. stage every bound list (independent loads, one round trip)
-    for (int x = lane; x < span; x += 32) {
-        const int p = x / Kq, e = x - p * Kq;
-        const int64_t part = p0 + p;
-        sA[x] = e < a.f.part_cnt[part * TILE + row] ? a.f.part_A[(part * Kq + e) * TILE + row]
-                                                     : kInf;
+    int incl = cnt;  // inclusive prefix of the list lengths over parts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int L = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - cnt;
+    for (int p = 0; p < parts; ++p) {
+        const int cp = __shfl_sync(0xffffffffu, cnt, p);
+        const int ep = __shfl_sync(0xffffffffu, excl, p);
+        for (int e = lane; e < cp; e += 32) sv[ep + e] = a.f.part_A[((p0 + p) * Kq + e) * TILE + row];
     }
     __syncwarp();
 
-    // 1. k-th smallest group minimum over all lists (k distinct references):
-    //    k-step tournament on the sorted list heads
-    int head = 0;
-    float hv = (lane < parts && cnt > 0) ? sA[lane * Kq] : kInf;
-    float ak = kInf;
-    for (int s = 0; s < k; ++s) {
-        float mv = hv;
-        int ml = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
-            const int ol = __shfl_xor_sync(0xffffffffu, ml, o);
-            if (ov < mv || (ov == mv && ol < ml)) {
-                mv = ov;
-                ml = ol;
+    // 1. k-th smallest (value, position) of the compacted lists
+    float B = kInf;
+    if (L >= k) {
+        for (int x = lane; x < L; x += 32) {
+            const float v = sv[x];
+            int c = 0;
+            for (int y = 0; y < L; ++y) {
+                const float w = sv[y];
+                c += (w < v || (w == v && y < x)) ? 1 : 0;
             }
+            if (c == k - 1) B = v;
         }
-        ak = mv;
-        if (lane == ml) {
-            ++head;
-            hv = head < cnt ? sA[lane * Kq + head] : kInf;
-        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
     }
     const Consts qc = load_consts(a.f, q);
-    const float tau = thresh(ak, qc);
+    const float tau = thresh(B, qc);
 
-    // 2. certificate: every group that ever passed a filter bound (>= tau) is
-    //    in its part's log, i.e. no log overflowed
-    const bool ok = __all_sync(0xffffffffu, nlog <= a.f.CG) && isfinite(tau);
+    // 2. certificate
+    bool ok = __all_sync(0xffffffffu, nlog <= a.f.CG) && isfinite(tau);
+
+    // 3. candidates: logged values <= tau
+    int nc = 0;
+    if (ok) {
+        for (int p = 0; p < parts; ++p) {
+            const int np = __shfl_sync(0xffffffffu, nlog, p);
+            const int64_t lq = ((p0 + p) * TILE + row) * a.f.CG;
+            for (int g0 = 0; g0 < np; g0 += 32) {
+                const int g = g0 + lane;
+                float w[8];
+                int c0 = 0;
+                if (g < np) {
+                    const float4 u = a.f.log_v[2 * (lq + g)], v = a.f.log_v[2 * (lq + g) + 1];
+                    w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+                    w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
+                    c0 = a.f.log_c[lq + g];
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w[e] = kInf;
+                }
+                const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
+                if (!__any_sync(0xffffffffu, gm <= tau)) continue;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const bool c = w[e] <= tau;
+                    const unsigned bal = __ballot_sync(0xffffffffu, c);
+                    const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+                    if (c && pos < RR_CAND) ci[pos] = c0 + e;
+                    nc += __popc(bal);
+                }
+            }
+        }
+        ok = nc <= RR_CAND && nc >= k;  // heavy ties beyond the fast path: exact kernel
+    }
     if (!ok) {
         if (lane == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
@@ -777,82 +881,42 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         }
         return;
     }
-
-    // 3. candidates with A <= tau, exact FP32 keys, exact top-k
-    WarpList<int64_t> LF{fk, fi, k};
-    LF.init(lane);
     __syncwarp();
+
+    // 4. exact FP32 keys of the candidates (lane-parallel, fixed coordinate order)
     const float* qrow = a.Q + q * a.d;
-    int taken = 0;   // candidates consumed so far (warp-uniform)
-    int myj = -1;    // reference index of this lane's pending candidate
-    // exact keys of the pending candidates (lane-parallel), then offer them
-    auto emit = [&]() {
-        float key = kInf;
-        int64_t gid = kSentinelIdx;
-        if (myj >= 0) {
-            const float* rrow = a.R + static_cast<int64_t>(myj) * a.d;
-            float acc = 0.f;
-            if ((a.d & 3) == 0) {
-                const float4* q4 = reinterpret_cast<const float4*>(qrow);
-                const float4* r4 = reinterpret_cast<const float4*>(rrow);
+    for (int c = lane; c < nc; c += 32) {
+        const float* rrow = a.R + static_cast<int64_t>(ci[c]) * a.d;
+        float acc = 0.f;
+        if ((a.d & 3) == 0) {
+            const float4* q4 = reinterpret_cast<const float4*>(qrow);
+            const float4* r4 = reinterpret_cast<const float4*>(rrow);
 #pragma unroll 4
-                for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
-                    const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
-                    acc = key_step<kL2>(acc, u.x, w.x);
-                    acc = key_step<kL2>(acc, u.y, w.y);
-                    acc = key_step<kL2>(acc, u.z, w.z);
-                    acc = key_step<kL2>(acc, u.w, w.w);
-                }
-            } else {
-                for (int cc = 0; cc < a.d; ++cc)
-                    acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
+            for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
+                const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
+                acc = key_step<kL2>(acc, u.x, w.x);
+                acc = key_step<kL2>(acc, u.y, w.y);
+                acc = key_step<kL2>(acc, u.z, w.z);
+                acc = key_step<kL2>(acc, u.w, w.w);
             }
-            key = acc;
-            gid = myj;
+        } else {
+            for (int cc = 0; cc < a.d; ++cc) acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
         }
-        float ck[1] = {key};
-        int64_t ci[1] = {gid};
-        LF.offer<1>(ck, ci, lane);
-        myj = -1;
-    };
-    // logged groups of every part: values <= tau are the candidates
-    for (int p = 0; p < parts; ++p) {
-        const int np = __shfl_sync(0xffffffffu, nlog, p);
-        const int64_t lq = ((p0 + p) * TILE + row) * a.f.CG;
-        for (int g0 = 0; g0 < np; g0 += 32) {
-            const int g = g0 + lane;
-            float w[8];
-            int c0 = 0;
-            if (g < np) {
-                const float4 u = a.f.log_v[2 * (lq + g)], v = a.f.log_v[2 * (lq + g) + 1];
-                w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
-                w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
-                c0 = a.f.log_c[lq + g];
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) w[e] = kInf;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const bool c = w[e] <= tau;
-                const unsigned bal = __ballot_sync(0xffffffffu, c);
-                if (bal == 0u) continue;
-                const int pos = taken + __popc(bal & ((1u << lane) - 1u));
-                const int j = c ? c0 + e : -1;
-                unsigned rem = bal;
-                while (rem) {
-                    const int src = __ffs(rem) - 1;
-                    rem &= rem - 1;
-                    const int pj = __shfl_sync(0xffffffffu, j, src);
-                    const int pp = __shfl_sync(0xffffffffu, pos, src);
-                    if ((pp & 31) == lane) myj = pj;
-                    if ((pp & 31) == 31) emit();  // 32 candidates assembled
-                }
-                taken += __popc(bal);
-            }
+        ck[c] = acc;
+    }
+    __syncwarp();
+
+    // 5. exact top-k: rank of every candidate under the (key, index) order
+    for (int c = lane; c < nc; c += 32) {
+        const float kc = ck[c];
+        const int jc = ci[c];
+        int r = 0;
+        for (int c2 = 0; c2 < nc; ++c2) r += pair_less(ck[c2], ci[c2], kc, jc) ? 1 : 0;
+        if (r < k) {
+            fk[r] = kc;
+            fi[r] = jc;
         }
     }
-    if (taken & 31) emit();
     __syncwarp();
     if (!a.raw_keys) finalize_list(fk, fi, k, kL2, lane);
     for (int t = lane; t < k; t += 32) {
@@ -1007,10 +1071,19 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
     {
         ProfileScope ps(stream, "prep_range_kernel");
-        range_kernel<<<static_cast<unsigned>((m + 63) / 64), 128, 0, stream>>>(dR, m, d, mnmx,
-                                                                                mnmx + d);
-        range_kernel<<<static_cast<unsigned>((n + 63) / 64), 128, 0, stream>>>(dQ, n, d, mnmx,
-                                                                                mnmx + d);
+        auto range = [&](const float* X, int64_t rows) {
+            const int vec = (d % 4 == 0) ? 4 : 1;
+            const int rpb = 256 / (d / vec);
+            const int64_t want = (rows + rpb * 8 - 1) / (rpb * 8);  // >= 8 rows per thread
+            const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+                1, std::min<int64_t>(want, 4 * kSmCount)));
+            if (vec == 4)
+                range_kernel<4><<<grid, 256, 0, stream>>>(X, rows, d, mnmx, mnmx + d);
+            else
+                range_kernel<1><<<grid, 256, 0, stream>>>(X, rows, d, mnmx, mnmx + d);
+        };
+        range(dR, m);
+        range(dQ, n);
     }
     KNN_LAUNCH_CHECK();
     note_launch();
@@ -1033,7 +1106,8 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     pr.norm = rnorm;
     {
         ProfileScope ps(stream, "prep_convert_refs");
-        convert_kernel<false><<<static_cast<unsigned>((m_pad + 7) / 8), 256, 0, stream>>>(pr);
+        convert_kernel<false><<<static_cast<unsigned>(std::min<int64_t>((m_pad + 7) / 8, 8 * kSmCount)),
+                                256, 0, stream>>>(pr);
     }
     KNN_LAUNCH_CHECK();
     pr.X = dQ;
@@ -1043,7 +1117,8 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     pr.qconst = qconst;
     {
         ProfileScope ps(stream, "prep_convert_queries");
-        convert_kernel<true><<<static_cast<unsigned>((n_pad + 7) / 8), 256, 0, stream>>>(pr);
+        convert_kernel<true><<<static_cast<unsigned>(std::min<int64_t>((n_pad + 7) / 8, 8 * kSmCount)),
+                               256, 0, stream>>>(pr);
     }
     KNN_LAUNCH_CHECK();
 
@@ -1133,8 +1208,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ra.out_idx = d_idx;
     ra.fb_count = fb;
     ra.fb_list = fb + 1;
-    const size_t rr_smem =
-        static_cast<size_t>(RR_WARPS) * (4 * S_max * L.Kq + static_cast<size_t>(k) * 12) + 16;
+    const size_t rr_smem = static_cast<size_t>(RR_WARPS) * rr_warp_bytes(S_max * L.Kq, k);
     {
         ProfileScope ps(stream, "rerank_kernel");
         rerank_kernel<<<static_cast<unsigned>((n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, rr_smem,
