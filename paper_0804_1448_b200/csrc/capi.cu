@@ -69,6 +69,33 @@ void check_point_set(const float* data, int64_t n, int64_t d, bool check_values)
     }
 }
 
+// Device-side PointSet value check (point_set.hpp:27-31): first index of a
+// non-finite coordinate (atomicMin), so the host API validates a device copy
+// in microseconds instead of scanning n*d values on one host core.
+__global__ void finite_scan_kernel(const float* X, int64_t count, unsigned long long* first) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += stride) {
+        if (!isfinite(__ldg(X + i))) atomicMin(first, static_cast<unsigned long long>(i));
+    }
+}
+
+// No CUDA device (e.g. a CPU-only CI box): validate on the host so argument
+// errors keep the reference's text; the search itself then fails loudly.
+bool device_present() {
+    static const bool present = [] {
+        int count = 0;
+        return cudaGetDeviceCount(&count) == cudaSuccess && count > 0;
+    }();
+    return present;
+}
+
+void throw_non_finite(unsigned long long i, int64_t d) {
+    throw InvalidArgument("PointSet: non-finite coordinate at point " +
+                          std::to_string(static_cast<int64_t>(i) / d) + ", dimension " +
+                          std::to_string(static_cast<int64_t>(i) % d));
+}
+
 // Metric::mahalanobis (metric.cpp:20-61): validate, Cholesky M = L L^T.
 std::vector<double> cholesky_or_throw(const double* M, int64_t d) {
     if (d <= 0) throw InvalidArgument("Metric: Mahalanobis dimension must be >= 1");
@@ -183,9 +210,19 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         const knn_b200_options& o = opts_or_default(opt, tmp);
         std::vector<double> chol;
         if (metric == kMahalanobis) chol = cholesky_or_throw(o.mahalanobis, o.mahalanobis_dim);
-        check_point_set(queries, n, dq, true);
-        check_point_set(references, m, dr, true);
-        check_search(dq, dr, m, k, o, metric);
+        // values are checked on the device below (Euclidean / L1 / Linf); the
+        // host scan only runs where the reference's error order needs it
+        const bool host_values = metric == kMahalanobis || !device_present();
+        check_point_set(queries, n, dq, host_values);
+        check_point_set(references, m, dr, host_values);
+        try {
+            check_search(dq, dr, m, k, o, metric);
+        } catch (const InvalidArgument&) {
+            // a PointSet error is raised at construction, before any bf_knn check
+            check_point_set(queries, n, dq, true);
+            check_point_set(references, m, dr, true);
+            throw;
+        }
         if (!out_dist || !out_idx) throw InvalidArgument("bf_knn: null output pointer");
 
         std::vector<float> wq, wr;
@@ -209,14 +246,30 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         sz.take<float>(static_cast<size_t>(m) * dr);
         sz.take<float>(static_cast<size_t>(n) * k);
         sz.take<int64_t>(static_cast<size_t>(n) * k);
+        sz.take<unsigned long long>(2);
         ctx.io.reserve(sz.used + 256);
         Carver cv{static_cast<char*>(ctx.io.base())};
         float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
         float* dR = cv.take<float>(static_cast<size_t>(m) * dr);
         float* dO = cv.take<float>(static_cast<size_t>(n) * k);
         int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
+        unsigned long long* dbad = cv.take<unsigned long long>(2);
         KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, q, sizeof(float) * n * dq, cudaMemcpyHostToDevice, s));
         KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * dr, cudaMemcpyHostToDevice, s));
+        if (!host_values) {
+            KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
+            const unsigned gq = static_cast<unsigned>(std::min<int64_t>((n * dq + 255) / 256, 1184));
+            const unsigned gr = static_cast<unsigned>(std::min<int64_t>((m * dr + 255) / 256, 1184));
+            finite_scan_kernel<<<gq, 256, 0, s>>>(dQ, n * dq, dbad);
+            KNN_LAUNCH_CHECK();
+            finite_scan_kernel<<<gr, 256, 0, s>>>(dR, m * dr, dbad + 1);
+            KNN_LAUNCH_CHECK();
+            unsigned long long bad[2];
+            KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+            KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+            if (bad[0] != ~0ull) throw_non_finite(bad[0], dq);
+            if (bad[1] != ~0ull) throw_non_finite(bad[1], dr);
+        }
         search_device(ctx, s, dQ, n, dR, m, dq, k, kernel_metric, o.path, o.raw_keys, 0, dO, dI);
         KNN_CUDA_CHECK(
             cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));

@@ -270,3 +270,24 @@ def test_tensor_path_is_used_and_certified(knn, oracle):
     tse = knn.bf_knn(Qd, Rs, 20, config=knn.BfConfig(path=knn.PATH_EXACT))
     assert (ts.index == tse.index).all() and (ts.distance == tse.distance).all()
     assert (ts.index == np.arange(20)[None, :]).all()
+
+
+@pytest.mark.gpu
+def test_non_finite_detected_on_device(knn, oracle):
+    """The host API validates coordinates on the device copy (point_set.hpp:27-31
+    text, first offending coordinate in row-major order)."""
+    R = oracle.uniform_f32(3000, 32, 41)
+    Q = oracle.uniform_f32(500, 32, 42)
+    Qb = Q.copy()
+    Qb[7, 3] = np.inf
+    Qb[9, 1] = np.nan
+    with pytest.raises(ValueError, match=r"^PointSet: non-finite coordinate at point 7, dimension 3$"):
+        knn.bf_knn(Qb, R, 5)
+    Rb = R.copy()
+    Rb[2999, 31] = -np.inf
+    with pytest.raises(ValueError, match=r"^PointSet: non-finite coordinate at point 2999, dimension 31$"):
+        knn.bf_knn(Q, Rb, 5)
+    # a clean search on the same context still works afterwards
+    t = knn.bf_knn(Q, R, 5)
+    ri, rd = oracle.knn(Q[:50], R, 5)
+    assert compare(t.index[:50], t.distance[:50], ri, rd, Q[:50], R, oracle=oracle).ok
