@@ -50,10 +50,9 @@ namespace knnb200 {
 namespace {
 
 constexpr int TILE = 128;          // queries per MMA tile (M) and references per tile (N)
-constexpr int EPI_WARPS = 8;       // two groups of four (one warp per TMEM lane quarter)
+constexpr int EPI_WARPS = 8;       // two sets of four (one warp per TMEM lane quarter)
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
-constexpr int NBUF = 4;            // TMEM accumulator buffers (4 x 128 columns = 512)
 constexpr int KEXTRA = 0;          // bound list K' >= k + KEXTRA
 constexpr int kLogGroups = 256;    // logged candidate groups per (query, CTA part)
 constexpr int MAX_KQ = 32;
@@ -298,7 +297,7 @@ struct FilterArgs {
     float4* log_v;         // [parts][128][CG][2] the 8 A values of each logged group
     int* log_c;            // [parts][128][CG] first reference index of each logged group
     int CG;                // log capacity (groups) per (part, query)
-    int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 1 ld+min, 2 no epilogue work
+    int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
 };
@@ -335,24 +334,57 @@ __device__ __forceinline__ float min3(float x, float y, float z) {
     return w;
 }
 
-constexpr int CAP = 6;         // per-lane buffered 8-column groups (smem planes [slot][thread])
-constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow, warpgroup 0 shrinks
+// Dev-only per-warp counters (make EXTRA=-DKNN_B200_FILTER_STATS, then run with
+// KNN_B200_FILTER_STATS=1); compiled out of the product build.
+#ifdef KNN_B200_FILTER_STATS
+constexpr bool kStats = true;
+#else
+constexpr bool kStats = false;
+#endif
+
+constexpr int CAP = 32;        // per-lane buffered group minima awaiting the bound list (smem);
+                               // drained once per tile (a tile pushes <= 16), off the TMEM path
+constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow by what warpgroup 0 frees
+// (the pool is the CTA's launch allocation: 2 x 128 x (232 - 168) = 128 x (168 - 40))
 constexpr int CTRL_REGS = 40;
 
-// Predicated append of one 8-value group to a lane's smem candidate buffer:
-// stores happen iff gm <= tf (inline PTX so the compiler cannot turn the
-// predicate into a branch).  a0/a1: the slot's two float4 plane addresses,
-// ai: its column-base address (shared window).
-__device__ __forceinline__ void push_group(float gm, float tf, uint32_t a0, uint32_t a1, uint32_t ai,
-                                           const float* w, int col) {
+// Predicated append of one 8-reference group (inline PTX so the predicate
+// never becomes a branch): if gm <= tf, the group minimum goes to the lane's
+// smem buffer (bound-list input, drained later) and, while the query's log
+// has room (room != 0), the 8 A values and the group's first reference index
+// go to the global group log (the re-rank's candidate source).
+__device__ __forceinline__ void push_group(float gm, float tf, uint32_t sg, int room, float4* lv,
+                                           int* lc, const float* w, int col) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.le.f32 p, %0, %1;\n\t"
-        "@p st.shared.v4.f32 [%2], {%5, %6, %7, %8};\n\t"
-        "@p st.shared.v4.f32 [%3], {%9, %10, %11, %12};\n\t"
-        "@p st.shared.b32 [%4], %13;\n\t}" ::"f"(gm),
-        "f"(tf), "r"(a0), "r"(a1), "r"(ai), "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]), "f"(w[4]),
-        "f"(w[5]), "f"(w[6]), "f"(w[7]), "r"(col)
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.le.f32 p, %0, %1;\n\t"
+        "setp.ne.and.s32 q, %3, 0, p;\n\t"
+        "@p st.shared.f32 [%2], %0;\n\t"
+        "@q st.global.v4.f32 [%4], {%6, %7, %8, %9};\n\t"
+        "@q st.global.v4.f32 [%4+16], {%10, %11, %12, %13};\n\t"
+        "@q st.global.b32 [%5], %14;\n\t}" ::"f"(gm),
+        "f"(tf), "r"(sg), "r"(room), "l"(lv), "l"(lc), "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]),
+        "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "r"(col)
         : "memory");
+}
+
+// no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~
+__device__ __forceinline__ void add_rnorm(float (&v)[32], const float* rn) {
+    const float4* nr = reinterpret_cast<const float4*>(rn);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float4 w = __ldg(nr + j);
+        v[4 * j] += w.x;
+        v[4 * j + 1] += w.y;
+        v[4 * j + 2] += w.z;
+        v[4 * j + 3] += w.w;
+    }
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
 }
 
 // The KR smallest group minima seen by this (query, CTA part), sorted
@@ -395,11 +427,11 @@ struct RegList {
 // Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
 // resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA,
 // one thread of warp 1 issues two M=128 N=128 MMA chains per reference tile
-// (one per query tile, accumulators in 2 x 2 TMEM buffers), and epilogue
-// group g (4 warps, one per TMEM lane quarter) owns query tile g of the pair:
-// thread = query row, all 128 columns of every tile.  So each query keeps ONE
-// candidate list per CTA that touches it (not one per column split), and each
-// reference tile fetched from L2 feeds two MMAs.
+// (one per query tile) into TMEM buffer (query tile g, unit parity b), and
+// epilogue set (g, b) -- 4 warps, one per TMEM lane quarter -- owns exactly
+// that buffer: thread = query row, all 128 columns of every other reference
+// tile.  16 epilogue warps (4 per SM sub-partition) hide the TMEM-load and
+// selection latencies; each query keeps one bound list per (CTA, parity).
 template <int KR>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
@@ -411,17 +443,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
     unsigned char* As = base;                // 2 query tiles
     unsigned char* Bs = base + 2 * KBB;      // stages x reference tile
-    // candidate groups: two float4 planes (values 0-3 / 4-7) + column base, [slot][thread]
-    float4* BA0 = reinterpret_cast<float4*>(Bs + a.stages * KBB);
-    float4* BA1 = BA0 + CAP * EPI_THREADS;
-    int* BI = reinterpret_cast<int*>(BA1 + CAP * EPI_THREADS);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(BI + CAP * EPI_THREADS);
+    float* GB = reinterpret_cast<float*>(Bs + a.stages * KBB);        // [CAP][512] group minima
+    uint64_t* sT = reinterpret_cast<uint64_t*>(GB + CAP * EPI_THREADS);  // [2][128] tagged bounds
+    uint64_t* sP = sT + 2 * TILE;                                       // [2][2][128] tagged kp-th
+    uint64_t* bars = sP + 4 * TILE;
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
     uint64_t* a_full = bars + 2 * a.stages;
     uint64_t* a_empty = a_full + 1;
-    uint64_t* tfull = a_full + 2;  // [group][buffer]
-    uint64_t* tempty = tfull + 4;  // [group][buffer]
+    uint64_t* tfull = a_full + 2;  // [query tile][parity]
+    uint64_t* tempty = tfull + 4;  // [query tile][parity]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
     const int warp = threadIdx.x >> 5;
@@ -443,6 +474,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         sm100::fence_mbar_init();
     }
+    for (int i = threadIdx.x; i < 6 * TILE; i += blockDim.x) sT[i] = ~0ull;  // no tag matches
     if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
     sm100::tc_fence_before();
     __syncthreads();
@@ -501,17 +533,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int64_t u = u_begin; u < u_end; ++u, ++t) {
                 if (p != cur_p) {
                     if (cur_p >= 0) sm100::mma_commit(a_empty);
-                    sm100::mbar_wait_sleep(a_full, a_par);
+                    sm100::mbar_wait(a_full, a_par);
                     a_par ^= 1u;
                     cur_p = p;
                 }
                 const int b = static_cast<int>(t & 1);
                 const uint32_t tpar = static_cast<uint32_t>((t >> 1) & 1);
-                sm100::mbar_wait_sleep(full + stage, phase);
+                sm100::mbar_wait(full + stage, phase);
                 sm100::tc_fence_after();
                 const uint32_t b0 = sm100::smem_u32(Bs + stage * KBB);
                 for (int g = 0; g < 2; ++g) {
-                    sm100::mbar_wait_sleep(tempty + 2 * g + b, tpar ^ 1u);
+                    sm100::mbar_wait(tempty + 2 * g + b, tpar ^ 1u);
                     sm100::tc_fence_after();
                     const uint32_t a0 = sm100::smem_u32(As + g * KBB);
                     const uint32_t dt = tmem + static_cast<uint32_t>((2 * g + b) * TILE);
@@ -542,57 +574,39 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int et = ew * 32 + lane;    // buffer column (0..255)
         const int row = quarter * 32 + lane;
         const int k = a.k;
-        constexpr uint32_t PLANE = CAP * EPI_THREADS * 16;  // bytes between the two value planes
-        const uint32_t sA0 = sm100::smem_u32(BA0) + static_cast<uint32_t>(et) * 16;
-        const uint32_t sI = sm100::smem_u32(BI) + static_cast<uint32_t>(et) * 4;
+        const uint32_t sg0 = sm100::smem_u32(GB) + static_cast<uint32_t>(et) * 4;
 
         RegList<KR> L;
         L.reset();
-        int cur_p = -1, qt = 0;
-        int nb = 0;        // buffered candidate groups
-        float T = kInf;    // own bound: thresh(k-th smallest A of this list)
-        float Tf = kInf;   // filter bound: min(T, other CTAs' bounds for this query)
+        int cur_p = -1;
+        int nb = 0;        // buffered group minima
+        float T = kInf;    // own bound: thresh(k-th smallest group minimum of this list)
+        float Tf = kInf;   // filter bound: min over every valid bound for this query
         unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
         Consts qc{};
         int64_t q = 0;
-        int64_t t = 0;
         int64_t part = 0;
-        float4* lv = nullptr;  // this (query, part)'s group log
-        int* lc = nullptr;
+        float4* lvp = nullptr;  // next slot of this (query, part)'s group log
+        int* lcp = nullptr;
         int ln = 0;            // groups logged so far (may exceed CG: overflow)
-        unsigned long long st_pushed = 0, st_ins = 0, st_drains = 0, st_rounds = 0;
+        unsigned long long st_drains = 0, st_rounds = 0;
         long long st_cyc_drain = 0, st_cyc_wait = 0;
-        const long long st_cyc0 = clock64();
+        const long long st_cyc0 = kStats ? clock64() : 0;
 
-        // Drain: one buffered group per lane per round.  A group whose minimum
-        // is still under the (possibly tightened) bound is inserted into the
-        // bound list by its minimum and appended whole to the query's global
-        // group log (the re-rank reads the candidates from there).  Then the
-        // bound is refreshed from this list and from the other CTAs' lists of
-        // the same query (global atomicMin, read one drain late so the load
-        // latency hides).
+        // Drain: one buffered group minimum per lane per round into the bound
+        // list, then refresh the bound from (1) this list, (2) the other
+        // parity's list of the same query (smem, tagged by pair), (3) the union
+        // of both lists' ceil(k/2)-th values, (4) other CTAs' lists (global
+        // atomicMin, read one drain late so the load latency hides).
 #define KNN_DRAIN()                                                                              \
     do {                                                                                         \
-        const long long c0_ = a.stats ? clock64() : 0;                                           \
-        if (a.stats) { ++st_drains; st_pushed += nb; }                                           \
+        const long long c0_ = (kStats && a.stats) ? clock64() : 0;                                           \
+        if (kStats && a.stats) ++st_drains;                                                                \
         const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
         _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
-            if (a.stats) ++st_rounds;                                                            \
-            if (j_ < nb) {                                                                       \
-                const float4 p_ = BA0[j_ * EPI_THREADS + et], q_ = BA1[j_ * EPI_THREADS + et];   \
-                const int c_ = BI[j_ * EPI_THREADS + et];                                        \
-                const float g_ = fminf(min3(min3(p_.x, p_.y, p_.z), min3(p_.w, q_.x, q_.y), q_.z), q_.w); \
-                if (g_ <= Tf) {                                                                  \
-                    L.insert(g_);                                                                \
-                    if (ln < a.CG) {                                                             \
-                        lv[2 * ln] = p_;                                                         \
-                        lv[2 * ln + 1] = q_;                                                     \
-                        lc[ln] = c_;                                                             \
-                    }                                                                            \
-                    ++ln;                                                                        \
-                    if (a.stats) ++st_ins;                                                       \
-                }                                                                                \
-            }                                                                                    \
+            if (kStats && a.stats) ++st_rounds;                                                            \
+            const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
+            if (g_ <= Tf) L.insert(g_);                                                          \
         }                                                                                        \
         nb = 0;                                                                                  \
         if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
@@ -600,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (T < kInf) atomicMin(a.tglob + q, enc(T));                                            \
         tg_pref = __ldcg(a.tglob + q);                                                           \
         Tf = tf_;                                                                                \
-        if (a.stats) st_cyc_drain += clock64() - c0_;                                            \
+        if (kStats && a.stats) st_cyc_drain += clock64() - c0_;                                            \
     } while (0)
 
 #define KNN_FLUSH()                                                                              \
@@ -613,43 +627,81 @@ __global__ void __launch_bounds__(THREADS, 1)
     } while (0)
 
         // One 32-column chunk, branch-free: the minimum of each 8-column group
-        // (FMNMX3), and every group whose minimum is under the lane's bound is
-        // appended whole (two 16-B stores + its column base) to the lane's
-        // buffer; the drain re-filters the 8 values.  A hit costs a few
-        // predicated stores instead of a divergent branch, which matters
-        // because with 32 queries per warp some lane hits in most chunks.
+        // (FMNMX3); every group whose minimum is under the lane's bound is
+        // pushed (predicated stores): its minimum to the smem buffer, its 8
+        // values to the global log.  With 32 queries per warp some lane hits
+        // in most chunks, so a hit must not cost a divergent branch.
 #define KNN_SCAN_CHUNK(vv, colb)                                                                 \
     do {                                                                                         \
-        if (__any_sync(0xffffffffu, nb > CAP - 4)) KNN_DRAIN();                                  \
+        float gm_[4];                                                                            \
+        bool any_ = false;                                                                       \
         _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                       \
             const float* w_ = vv + 8 * i_;                                                       \
-            const float gm_ = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]),   \
-                                         w_[6]), w_[7]);                                         \
-            const uint32_t o_ = static_cast<uint32_t>(nb) * (EPI_THREADS * 16);                  \
-            push_group(gm_, Tf, sA0 + o_, sA0 + PLANE + o_, sI + (o_ >> 2), w_, (colb) + 8 * i_); \
-            nb += gm_ <= Tf ? 1 : 0;                                                             \
+            gm_[i_] = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]), w_[6]),   \
+                            w_[7]);                                                              \
+            any_ |= gm_[i_] <= Tf;                                                               \
+        }                                                                                        \
+        if (__any_sync(0xffffffffu, any_)) { /* some lane pushes: ~half the chunks */           \
+            _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                   \
+                push_group(gm_[i_], Tf, sg0 + static_cast<uint32_t>(nb) * (EPI_THREADS * 4),     \
+                           ln < a.CG ? 1 : 0, lvp, lcp, vv + 8 * i_, (colb) + 8 * i_);           \
+                const int hit_ = gm_[i_] <= Tf ? 1 : 0;                                          \
+                nb += hit_;                                                                      \
+                ln += hit_;                                                                      \
+                lvp += hit_ ? 2 : 0;                                                             \
+                lcp += hit_;                                                                     \
+            }                                                                                    \
         }                                                                                        \
     } while (0)
 
         int p = static_cast<int>(u_begin / a.rtiles);
         int rt = static_cast<int>(u_begin % a.rtiles);
-        for (int64_t u = u_begin; u < u_end; ++u, ++t) {
+        const int nunits = static_cast<int>(u_end - u_begin);
+        const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(2 * grp * TILE);
+        auto wait_full = [&](int t) {
+            const long long cw_ = (kStats && a.stats) ? clock64() : 0;
+            sm100::mbar_wait(tfull + 2 * grp + (t & 1), static_cast<uint32_t>((t >> 1) & 1));
+            if (kStats && a.stats) st_cyc_wait += clock64() - cw_;
+            sm100::tc_fence_after();
+        };
+        auto release = [&](int t) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + (t & 1));
+        };
+
+        // Software pipeline over 32-column chunks, one TMEM load in flight
+        // (tcgen05.wait::ld waits for all): the load of chunk c+1 -- chunk 0
+        // of the next tile after chunk 3 -- overlaps the scan of chunk c.
+        uint32_t ra[32], rb[32];
+        if (a.mode != 2 && nunits > 0) {
+            wait_full(0);
+            sm100::tmem_ld_32x32b_x32(tlane, ra);
+            sm100::tmem_ld_wait();
+        }
+#define KNN_SCAN_REGS(rr, colb)                                                                  \
+    do {                                                                                         \
+        float v_[32];                                                                            \
+        _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
+        if (!a.fold) add_rnorm(v_, a.rnorm + (colb));                                            \
+        KNN_SCAN_CHUNK(v_, colb);                                                                \
+    } while (0)
+        for (int t = 0; t < nunits; ++t) {
             if (p != cur_p) {
                 if (cur_p >= 0) {
                     KNN_DRAIN();
                     KNN_FLUSH();
                 }
                 cur_p = p;
-                qt = 2 * p + grp;
+                const int qt = 2 * p + grp;
                 q = static_cast<int64_t>(qt) * TILE + row;
-                {
-                    const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
-                    part = static_cast<int64_t>(qt) * a.S_max + slot;
-                    const int64_t lq = (part * TILE + row) * a.CG;
-                    lv = a.log_v + 2 * lq;
-                    lc = a.log_c + lq;
-                    ln = 0;
-                }
+                const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
+                part = static_cast<int64_t>(qt) * a.S_max + slot;
+                const int64_t lq = (part * TILE + row) * a.CG;
+                lvp = a.log_v + 2 * lq;
+                lcp = a.log_c + lq;
+                ln = 0;
                 qc = load_consts(a, q);
                 L.reset();
                 T = kInf;
@@ -657,59 +709,29 @@ __global__ void __launch_bounds__(THREADS, 1)
                 Tf = dec_or_inf(tg_pref);
                 nb = 0;
             }
-            const int b = static_cast<int>(t & 1);
-            const long long cw_ = a.stats ? clock64() : 0;
-            sm100::mbar_wait(tfull + 2 * grp + b, static_cast<uint32_t>((t >> 1) & 1));
-            if (a.stats) st_cyc_wait += clock64() - cw_;
-            sm100::tc_fence_after();
-            const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                   static_cast<uint32_t>((2 * grp + b) * TILE);
             const int col_base = rt * TILE;
+            const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
             if (a.mode == 2) {
-                sm100::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
+                wait_full(t);
+                release(t);
             } else {
-                uint32_t r0[32], r1[32], r2[32], r3[32];
-                sm100::tmem_ld_32x32b_x32(taddr, r0);
-                sm100::tmem_ld_32x32b_x32(taddr + 32, r1);
-                sm100::tmem_ld_32x32b_x32(taddr + 64, r2);
-                sm100::tmem_ld_32x32b_x32(taddr + 96, r3);
+                sm100::tmem_ld_32x32b_x32(taddr + 32, rb);
+                KNN_SCAN_REGS(ra, col_base);
                 sm100::tmem_ld_wait();
-                sm100::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);  // registers hold the tile
-                float v[4][32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v[0][j] = __uint_as_float(r0[j]);
-                    v[1][j] = __uint_as_float(r1[j]);
-                    v[2][j] = __uint_as_float(r2[j]);
-                    v[3][j] = __uint_as_float(r3[j]);
-                }
-                if (!a.fold) {
-                    const float4* nr = reinterpret_cast<const float4*>(a.rnorm + col_base);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 w = __ldg(nr + 8 * c + j);
-                            v[c][4 * j] += w.x;
-                            v[c][4 * j + 1] += w.y;
-                            v[c][4 * j + 2] += w.z;
-                            v[c][4 * j + 3] += w.w;
-                        }
-                }
-                if (a.mode == 1) {
-                    float acc = kInf;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) acc = min3(acc, min3(v[0][j], v[1][j], v[2][j]), v[3][j]);
-                    if (acc == -1.f) a.sink[0] = acc;
-                } else {
-                    KNN_SCAN_CHUNK(v[0], col_base);
-                    KNN_SCAN_CHUNK(v[1], col_base + 32);
-                    KNN_SCAN_CHUNK(v[2], col_base + 64);
-                    KNN_SCAN_CHUNK(v[3], col_base + 96);
+                sm100::tmem_ld_32x32b_x32(taddr + 64, ra);
+                KNN_SCAN_REGS(rb, col_base + 32);
+                sm100::tmem_ld_wait();
+                sm100::tmem_ld_32x32b_x32(taddr + 96, rb);
+                KNN_SCAN_REGS(ra, col_base + 64);
+                sm100::tmem_ld_wait();
+                release(t);  // all four chunks of tile t are in registers
+                KNN_SCAN_REGS(rb, col_base + 96);
+                // drain after the release, so the MMA never waits on the list
+                if (__any_sync(0xffffffffu, nb > CAP - 16)) KNN_DRAIN();
+                if (t + 1 < nunits) {
+                    wait_full(t + 1);
+                    sm100::tmem_ld_32x32b_x32(tlane + static_cast<uint32_t>(((t + 1) & 1) * TILE), ra);
+                    sm100::tmem_ld_wait();
                 }
             }
             if (++rt == a.rtiles) {
@@ -717,19 +739,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ++p;
             }
         }
+#undef KNN_SCAN_REGS
         if (cur_p >= 0) {
             KNN_DRAIN();
             KNN_FLUSH();
         }
-        if (a.stats) {
-            const unsigned long long pushed = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_pushed));
-            const unsigned long long ins = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(st_ins));
+        if (kStats && a.stats) {
+            const unsigned long long lg = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(ln));
             if (lane == 0) {
-                atomicAdd(a.stats + 0, pushed);
+                atomicAdd(a.stats + 0, lg);
                 atomicAdd(a.stats + 1, st_drains);
                 atomicAdd(a.stats + 2, st_rounds);
-                atomicAdd(a.stats + 3, ins);
-                atomicAdd(a.stats + 4, static_cast<unsigned long long>(t));
+                atomicAdd(a.stats + 3, lg);
+                atomicAdd(a.stats + 4, static_cast<unsigned long long>(nunits));
                 atomicAdd(a.stats + 5, static_cast<unsigned long long>(st_cyc_drain));
                 atomicAdd(a.stats + 6, static_cast<unsigned long long>(st_cyc_wait));
                 atomicAdd(a.stats + 7, static_cast<unsigned long long>(clock64() - st_cyc0));
@@ -975,7 +997,7 @@ Layout layout_for(int d, int k) {
         ncol = L.d16;
     }
     const int kb_fold = (kfold + 63) / 64;
-    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 36;
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 + 6 * TILE * 8;
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
     auto stages_for = [&](int KB) {
         const size_t per = static_cast<size_t>(KB) * 16384;
@@ -1155,7 +1177,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.CG = CG;
     if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
     fa.sink = reinterpret_cast<float*>(log_n);
-    const bool want_stats = std::getenv("KNN_B200_FILTER_STATS") != nullptr;
+    const bool want_stats = kStats && std::getenv("KNN_B200_FILTER_STATS") != nullptr;
     if (want_stats) {
         KNN_CUDA_CHECK(cudaMallocAsync(&fa.stats, 8 * sizeof(unsigned long long), stream));
         KNN_CUDA_CHECK(cudaMemsetAsync(fa.stats, 0, 8 * sizeof(unsigned long long), stream));
