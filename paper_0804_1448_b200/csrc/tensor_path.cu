@@ -295,8 +295,9 @@ struct FilterArgs {
     int* part_cnt;         // [parts][128] entries in part_A
     int* log_n;            // [parts][128] groups logged (may exceed CG: overflow)
     float4* log_v;         // [parts][128][CG][2] the 8 A values of each logged group
-    int* log_c;            // [parts][128][CG] first reference index of each logged group
+    int2* log_h;           // [parts][128][CG] {group minimum bits, first reference index}
     int CG;                // log capacity (groups) per (part, query)
+    int drain_at;          // drain when a lane holds this many group minima (<= CAP - 16)
     int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
@@ -354,7 +355,7 @@ constexpr int CTRL_REGS = 40;
 // has room (room != 0), the 8 A values and the group's first reference index
 // go to the global group log (the re-rank's candidate source).
 __device__ __forceinline__ void push_group(float gm, float tf, uint32_t sg, int room, float4* lv,
-                                           int* lc, const float* w, int col) {
+                                           int2* lh, const float* w, int col) {
     asm volatile(
         "{\n\t.reg .pred p, q;\n\t"
         "setp.le.f32 p, %0, %1;\n\t"
@@ -362,8 +363,8 @@ __device__ __forceinline__ void push_group(float gm, float tf, uint32_t sg, int 
         "@p st.shared.f32 [%2], %0;\n\t"
         "@q st.global.v4.f32 [%4], {%6, %7, %8, %9};\n\t"
         "@q st.global.v4.f32 [%4+16], {%10, %11, %12, %13};\n\t"
-        "@q st.global.b32 [%5], %14;\n\t}" ::"f"(gm),
-        "f"(tf), "r"(sg), "r"(room), "l"(lv), "l"(lc), "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]),
+        "@q st.global.v2.b32 [%5], {%0, %14};\n\t}" ::"f"(gm),
+        "f"(tf), "r"(sg), "r"(room), "l"(lv), "l"(lh), "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]),
         "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "r"(col)
         : "memory");
 }
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int64_t q = 0;
         int64_t part = 0;
         float4* lvp = nullptr;  // next slot of this (query, part)'s group log
-        int* lcp = nullptr;
+        int2* lhp = nullptr;
         int ln = 0;            // groups logged so far (may exceed CG: overflow)
         unsigned long long st_drains = 0, st_rounds = 0;
         long long st_cyc_drain = 0, st_cyc_wait = 0;
@@ -644,12 +645,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (__any_sync(0xffffffffu, any_)) { /* some lane pushes: ~half the chunks */           \
             _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                   \
                 push_group(gm_[i_], Tf, sg0 + static_cast<uint32_t>(nb) * (EPI_THREADS * 4),     \
-                           ln < a.CG ? 1 : 0, lvp, lcp, vv + 8 * i_, (colb) + 8 * i_);           \
+                           ln < a.CG ? 1 : 0, lvp, lhp, vv + 8 * i_, (colb) + 8 * i_);           \
                 const int hit_ = gm_[i_] <= Tf ? 1 : 0;                                          \
                 nb += hit_;                                                                      \
                 ln += hit_;                                                                      \
                 lvp += hit_ ? 2 : 0;                                                             \
-                lcp += hit_;                                                                     \
+                lhp += hit_;                                                                     \
             }                                                                                    \
         }                                                                                        \
     } while (0)
@@ -700,7 +701,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 part = static_cast<int64_t>(qt) * a.S_max + slot;
                 const int64_t lq = (part * TILE + row) * a.CG;
                 lvp = a.log_v + 2 * lq;
-                lcp = a.log_c + lq;
+                lhp = a.log_h + lq;
                 ln = 0;
                 qc = load_consts(a, q);
                 L.reset();
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 release(t);  // all four chunks of tile t are in registers
                 KNN_SCAN_REGS(rb, col_base + 96);
                 // drain after the release, so the MMA never waits on the list
-                if (__any_sync(0xffffffffu, nb > CAP - 16)) KNN_DRAIN();
+                if (__any_sync(0xffffffffu, nb >= a.drain_at)) KNN_DRAIN();
                 if (t + 1 < nunits) {
                     wait_full(t + 1);
                     sm100::tmem_ld_32x32b_x32(tlane + static_cast<uint32_t>(((t + 1) & 1) * TILE), ra);
@@ -871,19 +872,20 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
             const int64_t lq = ((p0 + p) * TILE + row) * a.f.CG;
             for (int g0 = 0; g0 < np; g0 += 32) {
                 const int g = g0 + lane;
+                // group heads first (8 B each); the 8 values only where the
+                // group minimum is inside tau
+                const int2 hd = g < np ? a.f.log_h[lq + g] : make_int2(__float_as_int(kInf), 0);
+                const bool in = __int_as_float(hd.x) <= tau;
+                if (!__any_sync(0xffffffffu, in)) continue;
                 float w[8];
-                int c0 = 0;
-                if (g < np) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w[e] = kInf;
+                if (in) {
                     const float4 u = a.f.log_v[2 * (lq + g)], v = a.f.log_v[2 * (lq + g) + 1];
                     w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
                     w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
-                    c0 = a.f.log_c[lq + g];
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) w[e] = kInf;
                 }
-                const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
-                if (!__any_sync(0xffffffffu, gm <= tau)) continue;
+                const int c0 = hd.y;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const bool c = w[e] <= tau;
@@ -1063,7 +1065,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<int>(static_cast<size_t>(parts) * TILE);
     sz.take<int>(static_cast<size_t>(parts) * TILE);
     sz.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
-    sz.take<int>(static_cast<size_t>(parts) * TILE * CG);
+    sz.take<int2>(static_cast<size_t>(parts) * TILE * CG);
     sz.take<int>(static_cast<size_t>(n) + 1);
     sz.take<unsigned>(static_cast<size_t>(n_pad));
     ctx.arena.reserve(sz.used + 256);
@@ -1078,7 +1080,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     int* part_cnt = cv.take<int>(static_cast<size_t>(parts) * TILE);
     int* log_n = cv.take<int>(static_cast<size_t>(parts) * TILE);
     float4* log_v = cv.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
-    int* log_c = cv.take<int>(static_cast<size_t>(parts) * TILE * CG);
+    int2* log_h = cv.take<int2>(static_cast<size_t>(parts) * TILE * CG);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
     unsigned* gmax = mnmx + 2 * d;
@@ -1173,9 +1175,12 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.part_cnt = part_cnt;
     fa.log_n = log_n;
     fa.log_v = log_v;
-    fa.log_c = log_c;
+    fa.log_h = log_h;
     fa.CG = CG;
     if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
+    fa.drain_at = 8;
+    if (const char* e = std::getenv("KNN_B200_DRAIN_AT"))
+        fa.drain_at = std::max(1, std::min(CAP - 16, std::atoi(e)));
     fa.sink = reinterpret_cast<float*>(log_n);
     const bool want_stats = kStats && std::getenv("KNN_B200_FILTER_STATS") != nullptr;
     if (want_stats) {
