@@ -425,6 +425,130 @@ struct RegList {
     }
 };
 
+// The unit sequence every role of a filter CTA walks: its stream-K range
+// [u_begin, u_end) of (query-tile pair, reference tile) units, split into
+// segments of one pair each.  With W > 0 each segment is preceded by W "seed"
+// units: reference tiles spread evenly over the pair's whole reference range
+// (the large-k threshold estimate, filter_fixed_kernel).
+struct UnitSeq {
+    int64_t u, u_end, seg_end;
+    int rtiles, W, seed_left, p;
+    __device__ __forceinline__ void init(int64_t ub, int64_t ue, int rt, int w) {
+        u = ub;
+        u_end = ue;
+        rtiles = rt;
+        W = w;
+        if (u < u_end) begin_seg();
+    }
+    __device__ __forceinline__ void begin_seg() {
+        p = static_cast<int>(u / rtiles);
+        seg_end = min(u_end, static_cast<int64_t>(p + 1) * rtiles);
+        seed_left = W;
+    }
+    __device__ __forceinline__ bool more() const { return u < u_end; }
+    __device__ __forceinline__ bool seed() const { return seed_left > 0; }
+    __device__ __forceinline__ int tile() const {
+        return seed_left > 0 ? static_cast<int>(static_cast<int64_t>(W - seed_left) * rtiles / W)
+                             : static_cast<int>(u % rtiles);
+    }
+    __device__ __forceinline__ void next() {
+        if (seed_left > 0) {
+            --seed_left;
+            return;
+        }
+        if (++u < u_end && u == seg_end) begin_seg();
+    }
+};
+
+struct Pipe {  // one filter CTA's pipeline objects
+    unsigned char* As;   // 2 query tiles
+    unsigned char* Bs;   // stages x reference tile
+    int KBB;             // bytes of one 128-row operand tile
+    uint64_t *full, *empty, *a_full, *a_empty, *tfull, *tempty;
+    uint32_t tmem;
+};
+
+// warp 0, one elected thread: TMA loads of the query-tile pair (once per
+// segment) and of every unit's reference tile into the stage ring
+__device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUtensorMap* tr,
+                                              const FilterArgs& a, const Pipe& P, int64_t ub,
+                                              int64_t ue, int W) {
+    sm100::tma_prefetch(tq);
+    sm100::tma_prefetch(tr);
+    int stage = 0;
+    uint32_t phase = 0, a_par = 0;
+    int cur_p = -1;
+    UnitSeq sq;
+    sq.init(ub, ue, a.rtiles, W);
+    for (; sq.more(); sq.next()) {
+        if (sq.p != cur_p) {
+            if (cur_p >= 0) {
+                sm100::mbar_wait_sleep(P.a_empty, a_par);
+                a_par ^= 1u;
+            }
+            sm100::mbar_expect_tx(P.a_full, static_cast<uint32_t>(2 * P.KBB));
+            for (int g = 0; g < 2; ++g)
+                for (int kb = 0; kb < a.KB; ++kb)
+                    sm100::tma_load_2d(P.As + g * P.KBB + kb * 16384, tq, P.a_full, kb * 64,
+                                       (2 * sq.p + g) * TILE);
+            cur_p = sq.p;
+        }
+        sm100::mbar_wait_sleep(P.empty + stage, phase ^ 1u);
+        sm100::mbar_expect_tx(P.full + stage, static_cast<uint32_t>(P.KBB));
+        unsigned char* dst = P.Bs + stage * P.KBB;
+        const int rt = sq.tile();
+        for (int kb = 0; kb < a.KB; ++kb)
+            sm100::tma_load_2d(dst + kb * 16384, tr, P.full + stage, kb * 64, rt * TILE);
+        if (++stage == a.stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
+// warp 1, one elected thread: per unit two M=128 N=128 MMA chains (one per
+// query tile) into TMEM buffer [query tile][unit parity]
+__device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int64_t ub, int64_t ue,
+                                         int W) {
+    const uint32_t idesc = sm100::idesc_f16_f32(TILE, TILE);
+    int stage = 0;
+    uint32_t phase = 0, a_par = 0;
+    int cur_p = -1;
+    int64_t t = 0;
+    UnitSeq sq;
+    sq.init(ub, ue, a.rtiles, W);
+    for (; sq.more(); sq.next(), ++t) {
+        if (sq.p != cur_p) {
+            if (cur_p >= 0) sm100::mma_commit(P.a_empty);
+            sm100::mbar_wait(P.a_full, a_par);
+            a_par ^= 1u;
+            cur_p = sq.p;
+        }
+        const int b = static_cast<int>(t & 1);
+        const uint32_t tpar = static_cast<uint32_t>((t >> 1) & 1);
+        sm100::mbar_wait(P.full + stage, phase);
+        sm100::tc_fence_after();
+        const uint32_t b0 = sm100::smem_u32(P.Bs + stage * P.KBB);
+        for (int g = 0; g < 2; ++g) {
+            sm100::mbar_wait(P.tempty + 2 * g + b, tpar ^ 1u);
+            sm100::tc_fence_after();
+            const uint32_t a0 = sm100::smem_u32(P.As + g * P.KBB);
+            const uint32_t dt = P.tmem + static_cast<uint32_t>((2 * g + b) * TILE);
+            for (int ks = 0; ks < a.nslices; ++ks) {
+                const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
+                sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off), sm100::sdesc_k_sw128(b0 + off),
+                                  idesc, ks > 0 ? 1u : 0u);
+            }
+            sm100::mma_commit(P.tfull + 2 * g + b);
+        }
+        sm100::mma_commit(P.empty + stage);
+        if (++stage == a.stages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
 // Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
 // resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA,
 // one thread of warp 1 issues two M=128 N=128 MMA chains per reference tile
@@ -483,89 +607,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
+    const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer ----
-        if (sm100::elect_one()) {
-            sm100::tma_prefetch(&tq);
-            sm100::tma_prefetch(&tr);
-            int stage = 0;
-            uint32_t phase = 0, a_par = 0;
-            int cur_p = -1;
-            int p = static_cast<int>(u_begin / a.rtiles);
-            int rt = static_cast<int>(u_begin % a.rtiles);
-            for (int64_t u = u_begin; u < u_end; ++u) {
-                if (p != cur_p) {
-                    if (cur_p >= 0) {
-                        sm100::mbar_wait_sleep(a_empty, a_par);
-                        a_par ^= 1u;
-                    }
-                    sm100::mbar_expect_tx(a_full, static_cast<uint32_t>(2 * KBB));
-                    for (int g = 0; g < 2; ++g)
-                        for (int kb = 0; kb < a.KB; ++kb)
-                            sm100::tma_load_2d(As + g * KBB + kb * 16384, &tq, a_full, kb * 64,
-                                               (2 * p + g) * TILE);
-                    cur_p = p;
-                }
-                sm100::mbar_wait_sleep(empty + stage, phase ^ 1u);
-                sm100::mbar_expect_tx(full + stage, static_cast<uint32_t>(KBB));
-                unsigned char* dst = Bs + stage * KBB;
-                for (int kb = 0; kb < a.KB; ++kb)
-                    sm100::tma_load_2d(dst + kb * 16384, &tr, full + stage, kb * 64, rt * TILE);
-                if (++stage == a.stages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                if (++rt == a.rtiles) {
-                    rt = 0;
-                    ++p;
-                }
-            }
-        }
+        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, 0);
     } else if (warp == 1) {
-        // ------------------------------------------------- MMA issuer -----
-        if (sm100::elect_one()) {
-            const uint32_t idesc = sm100::idesc_f16_f32(TILE, TILE);
-            int stage = 0;
-            uint32_t phase = 0, a_par = 0;
-            int cur_p = -1;
-            int64_t t = 0;
-            int p = static_cast<int>(u_begin / a.rtiles);
-            int rt = static_cast<int>(u_begin % a.rtiles);
-            for (int64_t u = u_begin; u < u_end; ++u, ++t) {
-                if (p != cur_p) {
-                    if (cur_p >= 0) sm100::mma_commit(a_empty);
-                    sm100::mbar_wait(a_full, a_par);
-                    a_par ^= 1u;
-                    cur_p = p;
-                }
-                const int b = static_cast<int>(t & 1);
-                const uint32_t tpar = static_cast<uint32_t>((t >> 1) & 1);
-                sm100::mbar_wait(full + stage, phase);
-                sm100::tc_fence_after();
-                const uint32_t b0 = sm100::smem_u32(Bs + stage * KBB);
-                for (int g = 0; g < 2; ++g) {
-                    sm100::mbar_wait(tempty + 2 * g + b, tpar ^ 1u);
-                    sm100::tc_fence_after();
-                    const uint32_t a0 = sm100::smem_u32(As + g * KBB);
-                    const uint32_t dt = tmem + static_cast<uint32_t>((2 * g + b) * TILE);
-                    for (int ks = 0; ks < a.nslices; ++ks) {
-                        const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
-                        sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off),
-                                          sm100::sdesc_k_sw128(b0 + off), idesc, ks > 0 ? 1u : 0u);
-                    }
-                    sm100::mma_commit(tfull + 2 * g + b);
-                }
-                sm100::mma_commit(empty + stage);
-                if (++stage == a.stages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                if (++rt == a.rtiles) {
-                    rt = 0;
-                    ++p;
-                }
-            }
-        }
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0);
     } else if (warp >= 4) {
         // ------------------------------------------------- epilogue -------
         sm100::reg_alloc<EPI_REGS>();
