@@ -55,6 +55,7 @@ constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
 constexpr int KEXTRA = 0;          // bound list K' >= k + KEXTRA
 constexpr int kLogGroups = 256;    // logged candidate groups per (query, CTA part)
+constexpr int kMaxLargeK = 1024;   // k > MAX_KQ: fixed-threshold filter + block selection
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
 
@@ -301,6 +302,14 @@ struct FilterArgs {
     int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
+    // large-k (filter_fixed_kernel): seed tiles per segment, per-query
+    // threshold T0, compact value log {A, reference index} of capacity CV
+    int W;
+    int seed_off;          // 0 / 1: interleaved seed tile positions (retry uses fresh tiles)
+    int seed_rank;         // T0 = thresh(seed_rank-th smallest seed group minimum)
+    float* t0;             // [n_pad]
+    float2* vlog;          // [parts][128][CV]
+    int CV;
 };
 
 __device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
@@ -432,12 +441,13 @@ struct RegList {
 // (the large-k threshold estimate, filter_fixed_kernel).
 struct UnitSeq {
     int64_t u, u_end, seg_end;
-    int rtiles, W, seed_left, p;
-    __device__ __forceinline__ void init(int64_t ub, int64_t ue, int rt, int w) {
+    int rtiles, W, seed_left, p, off;
+    __device__ __forceinline__ void init(int64_t ub, int64_t ue, int rt, int w, int seed_off = 0) {
         u = ub;
         u_end = ue;
         rtiles = rt;
         W = w;
+        off = seed_off;
         if (u < u_end) begin_seg();
     }
     __device__ __forceinline__ void begin_seg() {
@@ -448,8 +458,9 @@ struct UnitSeq {
     __device__ __forceinline__ bool more() const { return u < u_end; }
     __device__ __forceinline__ bool seed() const { return seed_left > 0; }
     __device__ __forceinline__ int tile() const {
-        return seed_left > 0 ? static_cast<int>(static_cast<int64_t>(W - seed_left) * rtiles / W)
-                             : static_cast<int>(u % rtiles);
+        return seed_left > 0
+                   ? static_cast<int>((2LL * (W - seed_left) + off) * rtiles / (2LL * W))
+                   : static_cast<int>(u % rtiles);
     }
     __device__ __forceinline__ void next() {
         if (seed_left > 0) {
@@ -479,7 +490,7 @@ __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUten
     uint32_t phase = 0, a_par = 0;
     int cur_p = -1;
     UnitSeq sq;
-    sq.init(ub, ue, a.rtiles, W);
+    sq.init(ub, ue, a.rtiles, W, a.seed_off);
     for (; sq.more(); sq.next()) {
         if (sq.p != cur_p) {
             if (cur_p >= 0) {
@@ -516,7 +527,7 @@ __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int
     int cur_p = -1;
     int64_t t = 0;
     UnitSeq sq;
-    sq.init(ub, ue, a.rtiles, W);
+    sq.init(ub, ue, a.rtiles, W, a.seed_off);
     for (; sq.more(); sq.next(), ++t) {
         if (sq.p != cur_p) {
             if (cur_p >= 0) sm100::mma_commit(P.a_empty);
@@ -817,6 +828,391 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
+// Large k (k > 32): one filter pass with a FIXED per-query threshold.  Each
+// segment starts with W seed units (reference tiles spread over the pair's
+// whole reference range, filter_fixed_kernel only): every group minimum of
+// the seed goes into a 32-entry list and T0 = thresh(list[seed_rank-1]) is an
+// estimate of thresh(A_(c*k)).  The main units then log every value A <= T0
+// (compact {A, index} records, predicated stores).  T0 is only an estimate;
+// the selection kernel certifies it (at least k logged values and
+// thresh(A_(k)) <= T0, no log overflow) and sends the rest to the exact path.
+template <int DUMMY>
+__global__ void __launch_bounds__(THREADS, 1)
+    filter_fixed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                        FilterArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int KBB = a.KB * 16384;
+    unsigned char* As = base;
+    unsigned char* Bs = base + 2 * KBB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + a.stages * KBB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + a.stages;
+    uint64_t* a_full = bars + 2 * a.stages;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* tfull = a_full + 2;
+    uint64_t* tempty = tfull + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int64_t u_begin = unit_start(a.U, a.G, cta);
+    const int64_t u_end = unit_start(a.U, a.G, cta + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            sm100::mbar_init(full + s, 1);
+            sm100::mbar_init(empty + s, 1);
+        }
+        sm100::mbar_init(a_full, 1);
+        sm100::mbar_init(a_empty, 1);
+        for (int b = 0; b < 4; ++b) {
+            sm100::mbar_init(tfull + b, 1);
+            sm100::mbar_init(tempty + b, 4);
+        }
+        sm100::fence_mbar_init();
+    }
+    if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
+    const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
+    if (warp == 0) {
+        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, a.W);
+    } else if (warp == 1) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W);
+    } else if (warp >= 4) {
+        sm100::reg_alloc<EPI_REGS>();
+        const int ew = warp - 4;
+        const int grp = ew >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(2 * grp * TILE);
+        RegList<32> S;  // seed: the 32 smallest seed group minima
+        S.reset();
+        float T0 = kInf;
+        Consts qc{};
+        int64_t q = 0, part = 0;
+        float2* vlp = nullptr;
+        int ln = 0;
+        int cur_p = -1;
+        bool was_seed = false;
+        int64_t t = 0;
+        UnitSeq sq;
+        sq.init(u_begin, u_end, a.rtiles, a.W, a.seed_off);
+        auto finish = [&]() {
+            a.log_n[part * TILE + row] = ln;
+        };
+        for (; sq.more(); sq.next(), ++t) {
+            if (sq.p != cur_p) {
+                if (cur_p >= 0) finish();
+                cur_p = sq.p;
+                const int qt = 2 * sq.p + grp;
+                q = static_cast<int64_t>(qt) * TILE + row;
+                const int slot = cta - first_cta_of(static_cast<int64_t>(sq.p) * a.rtiles, a.U, a.G);
+                part = static_cast<int64_t>(qt) * a.S_max + slot;
+                vlp = a.vlog + (part * TILE + row) * a.CV;
+                ln = 0;
+                qc = load_consts(a, q);
+                S.reset();
+                T0 = kInf;
+            }
+            const bool seed = sq.seed();
+            if (!seed && was_seed) {  // seed complete: fix the segment's threshold
+                T0 = thresh(S.kth(a.seed_rank), qc);
+                if (lane < 32) a.t0[q] = T0;  // identical from every CTA of the pair
+            }
+            was_seed = seed;
+            const int b = static_cast<int>(t & 1);
+            sm100::mbar_wait(tfull + 2 * grp + b, static_cast<uint32_t>((t >> 1) & 1));
+            sm100::tc_fence_after();
+            const uint32_t taddr = tlane + static_cast<uint32_t>(b * TILE);
+            const int col_base = sq.tile() * TILE;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                uint32_t r0[32], r1[32];
+                sm100::tmem_ld_32x32b_x32(taddr + h * 64, r0);
+                sm100::tmem_ld_32x32b_x32(taddr + h * 64 + 32, r1);
+                sm100::tmem_ld_wait();
+                if (h == 1) {
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
+                }
+                float v[2][32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    v[0][j] = __uint_as_float(r0[j]);
+                    v[1][j] = __uint_as_float(r1[j]);
+                }
+                const int cb = col_base + h * 64;
+                if (!a.fold) {
+                    add_rnorm(v[0], a.rnorm + cb);
+                    add_rnorm(v[1], a.rnorm + cb + 32);
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const float* w = v[c] + 8 * g;
+                        const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]),
+                                               w[7]);
+                        if (seed) {
+                            S.insert(gm);
+                        } else if (__any_sync(0xffffffffu, gm <= T0)) {
+                            const int col = cb + 32 * c + 8 * g;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const int room = ln < a.CV ? 1 : 0;
+                                asm volatile(
+                                    "{\n\t.reg .pred p, q;\n\t"
+                                    "setp.le.f32 p, %0, %1;\n\t"
+                                    "setp.ne.and.s32 q, %2, 0, p;\n\t"
+                                    "@q st.global.v2.b32 [%3], {%0, %4};\n\t}" ::"f"(w[e]),
+                                    "f"(T0), "r"(room), "l"(vlp), "r"(col + e)
+                                    : "memory");
+                                const int hit = w[e] <= T0 ? 1 : 0;
+                                vlp += hit;
+                                ln += hit;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (cur_p >= 0) finish();
+    }
+
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, 512);
+    }
+}
+
+// Large-k selection, one 256-thread block per query: gather the query's
+// logged {A, index} values, bitonic-sort them by A, A_(k) = k-th; certify
+// (>= k logged, no overflow, thresh(A_(k)) <= T0); exact FP32 keys of every
+// value <= thresh(A_(k)); bitonic sort by (key, index); top k.
+constexpr int LK_THREADS = 256;
+#ifndef KNN_DBG_LARGE
+#define KNN_DBG_LARGE 0
+#endif
+
+__device__ void bitonic_sort_kv(float* key, int* idx, int N) {  // N power of two, block-wide
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < (N >> 1); i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const float ka = key[lo], kb = key[hi];
+                const int ia = idx[lo], ib = idx[hi];
+                const bool gt = pair_less(kb, ib, ka, ia);  // (a > b)
+                if (gt == up) {
+                    key[lo] = kb;
+                    key[hi] = ka;
+                    idx[lo] = ib;
+                    idx[hi] = ia;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// k-th smallest (1-based) of x[0..n) (finite floats), block-wide radix select
+// on enc() bits, most significant digit first.  hist: 256 shared counters.
+__device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist, int* scratch) {
+    unsigned prefix = 0, mask = 0;
+    int want = k;  // rank still to find among keys matching prefix
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
+        __syncthreads();
+        // warp-aggregated increments: the leading digits of nearby keys
+        // coincide, so plain atomics would serialise on one or two bins
+        for (int e0 = 0; e0 < n; e0 += blockDim.x) {
+            const int e = e0 + threadIdx.x;
+            int bin = -1;
+            if (e < n) {
+                const unsigned u = enc(x[e]);
+                if ((u & mask) == prefix) bin = static_cast<int>((u >> shift) & 255u);
+            }
+            const unsigned same = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && (__ffs(same) - 1) == (threadIdx.x & 31))
+                atomicAdd(hist + bin, static_cast<unsigned>(__popc(same)));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0, b = 0;
+            for (; b < 256; ++b) {
+                if (acc + static_cast<int>(hist[b]) >= want) break;
+                acc += static_cast<int>(hist[b]);
+            }
+            scratch[0] = b;
+            scratch[1] = want - acc;
+        }
+        __syncthreads();
+        const unsigned b = static_cast<unsigned>(scratch[0]);
+        want = scratch[1];
+        prefix |= b << shift;
+        mask |= 255u << shift;
+        __syncthreads();
+    }
+    return dec(prefix);
+}
+
+struct LargeArgs {
+    const float* Q;
+    const float* R;
+    int64_t n;
+    int d, k, S_max, NC;     // NC: smem capacity (power of two)
+    FilterArgs f;
+    int raw_keys;
+    int64_t index_base;
+    float* out;
+    int64_t* out_idx;
+    int* fb_count;
+    int* fb_list;
+};
+
+__global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
+    int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
+    __shared__ int s_off[33];
+    __shared__ int s_cnt;
+    __shared__ int s_sel[2];
+    __shared__ unsigned s_hist[256];
+    const int64_t q = blockIdx.x;
+    const int qt = static_cast<int>(q / TILE), row = static_cast<int>(q % TILE);
+    const int64_t p0 = static_cast<int64_t>(qt) * a.S_max;
+    const int k = a.k;
+    if (threadIdx.x == 0) {
+        int off = 0;
+        bool over = false;
+        for (int p = 0; p < a.S_max; ++p) {
+            const int np = a.f.log_n[(p0 + p) * TILE + row];
+            over |= np > a.f.CV;
+            s_off[p] = off;
+            off += min(np, a.f.CV);
+        }
+        s_off[a.S_max] = off;
+        s_cnt = over ? -1 : off;
+    }
+    __syncthreads();
+    const int total = s_cnt;
+    const float T0 = a.f.t0[q];
+    bool ok = total >= k && total <= a.NC;
+    float tau = kInf;
+    int nc = 0;
+    if (ok) {
+        for (int p = 0; p < a.S_max; ++p) {
+            const int o = s_off[p], np = s_off[p + 1] - o;
+            const float2* src = a.f.vlog + ((p0 + p) * TILE + row) * a.f.CV;
+            for (int e = threadIdx.x; e < np; e += blockDim.x) {
+                const float2 r = src[e];
+                sk[o + e] = r.x;
+                si[o + e] = __float_as_int(r.y);
+            }
+        }
+        __syncthreads();
+        // A_(k) by radix select on the order-preserving key bits (4 x 8-bit
+        // digits, block histograms), no sort
+        const float ak = block_kth_smallest(sk, total, k, s_hist, s_sel);
+        const Consts qc = load_consts(a.f, q);
+        tau = thresh(ak, qc);
+        ok = tau <= T0;  // every reference with A <= tau was logged
+        if (ok) {
+            // compact the candidates (A <= tau) to the front, any order
+            if (threadIdx.x == 0) s_cnt = 0;
+            __syncthreads();
+            int mine[32];  // total <= NC <= 32 * LK_THREADS: a thread owns <= 32 entries
+            int nm = 0;
+            for (int e = threadIdx.x; e < total; e += blockDim.x)
+                if (sk[e] <= tau) mine[nm++] = si[e];
+            __syncthreads();
+            const int base = atomicAdd(&s_cnt, nm);
+            for (int j = 0; j < nm; ++j) si[base + j] = mine[j];
+            __syncthreads();
+            nc = s_cnt;
+        }
+    }
+    if (!ok) {
+        if (threadIdx.x == 0) {
+            const int slot = atomicAdd(a.fb_count, 1);
+            a.fb_list[slot] = static_cast<int>(q);
+            if (KNN_DBG_LARGE && slot < 8)
+                printf("[select_large] q=%lld total=%d k=%d NC=%d tau=%g T0=%g nc=%d\n",
+                       static_cast<long long>(q), total, k, a.NC, tau, T0, nc);
+        }
+        return;
+    }
+    // exact keys of the nc candidates (their indices are si[0..nc))
+    const float* qrow = a.Q + q * a.d;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const float* rrow = a.R + static_cast<int64_t>(si[c]) * a.d;
+        float acc = 0.f;
+        if ((a.d & 3) == 0) {
+            const float4* q4 = reinterpret_cast<const float4*>(qrow);
+            const float4* r4 = reinterpret_cast<const float4*>(rrow);
+#pragma unroll 4
+            for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
+                const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
+                acc = key_step<kL2>(acc, u.x, w.x);
+                acc = key_step<kL2>(acc, u.y, w.y);
+                acc = key_step<kL2>(acc, u.z, w.z);
+                acc = key_step<kL2>(acc, u.w, w.w);
+            }
+        } else {
+            for (int cc = 0; cc < a.d; ++cc) acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
+        }
+        sk[c] = acc;
+    }
+    int N2 = 1;
+    while (N2 < nc) N2 <<= 1;
+    for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
+        sk[e] = kInf;
+        si[e] = 0x7fffffff;
+    }
+    bitonic_sort_kv(sk, si, N2);
+    // finalize: sqrt, then equal reported distances in ascending index order
+    if (!a.raw_keys) {
+        for (int t = threadIdx.x; t < k; t += blockDim.x) sk[t] = __fsqrt_rn(sk[t]);
+        __syncthreads();
+        // equal reported distances in ascending index order: each run of
+        // equal distances (keys were ascending, so runs are contiguous and
+        // short) is insertion-sorted by the thread owning its first slot
+        for (int t = threadIdx.x; t < k; t += blockDim.x) {
+            if (t > 0 && sk[t - 1] == sk[t]) continue;
+            int e = t + 1;
+            while (e < k && sk[e] == sk[t]) ++e;
+            for (int x = t + 1; x < e; ++x) {
+                const int j = si[x];
+                int u = x;
+                while (u > t && si[u - 1] > j) {
+                    si[u] = si[u - 1];
+                    --u;
+                }
+                si[u] = j;
+            }
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        a.out[q * k + t] = sk[t];
+        a.out_idx[q * k + t] = a.index_base + si[t];
+    }
+}
+
 // -------------------------------------------------------------- re-rank ----
 struct RerankArgs {
     const float* Q;        // original fp32 n x d
@@ -1071,14 +1467,14 @@ Layout layout_for(int d, int k) {
 }  // namespace
 
 bool tensor_path_supported(int64_t n, int64_t m, int d, int k) {
-    if (d < 1 || d > 128 || k < 1 || k + KEXTRA > MAX_KQ) return false;
+    if (d < 1 || d > 128 || k < 1 || k > kMaxLargeK) return false;
     if (m < k || n < 1 || m > (1LL << 30)) return false;
     return layout_for(d, k).stages >= 2;
 }
 
 void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
-                     float* d_out, int64_t* d_idx) {
+                     float* d_out, int64_t* d_idx, int margin, bool retry) {
     const Layout L = layout_for(d, k);
     const int pairs = static_cast<int>((n + 2 * TILE - 1) / (2 * TILE));
     const int qtiles = 2 * pairs;  // the last tile of the last pair may be all padding
@@ -1106,14 +1502,20 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<float4>(static_cast<size_t>(n_pad));
     sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
     sz.take<float>(static_cast<size_t>(d) + 1);
-    const int CG = kLogGroups;
-    sz.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
+    const bool large = k > MAX_KQ;
+    const int CG = large ? 0 : kLogGroups;
+    // large k: T0 ~ the (2k)-th smallest A; log room for twice that per part
+    const int CV = large ? 2 * margin * k + 256 : 0;
+    const int64_t np_list = large ? 0 : parts;
+    sz.take<float>(static_cast<size_t>(np_list) * L.Kq * TILE);
     sz.take<int>(static_cast<size_t>(parts) * TILE);
     sz.take<int>(static_cast<size_t>(parts) * TILE);
     sz.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
     sz.take<int2>(static_cast<size_t>(parts) * TILE * CG);
     sz.take<int>(static_cast<size_t>(n) + 1);
     sz.take<unsigned>(static_cast<size_t>(n_pad));
+    sz.take<float>(large ? static_cast<size_t>(n_pad) : 0);
+    sz.take<float2>(static_cast<size_t>(parts) * TILE * CV);
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -1122,13 +1524,15 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     float4* qconst = cv.take<float4>(static_cast<size_t>(n_pad));
     unsigned* mnmx = cv.take<unsigned>(2 * static_cast<size_t>(d) + 2);
     float* mu = cv.take<float>(static_cast<size_t>(d) + 1);
-    float* part_A = cv.take<float>(static_cast<size_t>(parts) * L.Kq * TILE);
+    float* part_A = cv.take<float>(static_cast<size_t>(np_list) * L.Kq * TILE);
     int* part_cnt = cv.take<int>(static_cast<size_t>(parts) * TILE);
     int* log_n = cv.take<int>(static_cast<size_t>(parts) * TILE);
     float4* log_v = cv.take<float4>(static_cast<size_t>(parts) * TILE * CG * 2);
     int2* log_h = cv.take<int2>(static_cast<size_t>(parts) * TILE * CG);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
+    float* t0 = cv.take<float>(large ? static_cast<size_t>(n_pad) : 0);
+    float2* vlog = cv.take<float2>(static_cast<size_t>(parts) * TILE * CV);
     unsigned* gmax = mnmx + 2 * d;
     float* scale = mu + d;
 
@@ -1241,6 +1645,56 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         ProfileScope ps(stream, "tc_filter_kernel");
         kern<<<G, THREADS, L.smem, stream>>>(tq, tr, fa);
     };
+    if (large) {
+        // seed: W tiles whose 32nd smallest group minimum estimates the
+        // (margin*k)-th smallest A (rank ~ m * 32 / (128 W)), W >= 2
+        fa.seed_rank = 32;
+        fa.W = static_cast<int>(std::min<int64_t>(
+            rtiles, std::max<int64_t>(2, (m + 4LL * margin * k - 1) / (4LL * margin * k))));
+        fa.seed_off = retry ? 1 : 0;
+        fa.t0 = t0;
+        fa.vlog = vlog;
+        fa.CV = CV;
+        const size_t smem_fixed = 1024 + 512 + static_cast<size_t>(L.KB) * 16384 *
+                                                   (2 + std::min(L.stages + 2, 6));
+        const int stages_fixed = std::min(L.stages + 2, 6);
+        fa.stages = stages_fixed;
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(filter_fixed_kernel<0>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem_fixed)));
+        {
+            ProfileScope ps(stream, "tc_filter_fixed_kernel");
+            filter_fixed_kernel<0><<<G, THREADS, smem_fixed, stream>>>(tq, tr, fa);
+        }
+        KNN_LAUNCH_CHECK();
+        LargeArgs la{};
+        la.Q = dQ;
+        la.R = dR;
+        la.n = n;
+        la.d = d;
+        la.k = k;
+        la.S_max = S_max;
+        int NC = 1;
+        while (NC < 2 * margin * k) NC <<= 1;
+        NC = std::min(NC, 32 * LK_THREADS);
+        la.NC = NC;
+        la.f = fa;
+        la.raw_keys = raw_keys;
+        la.index_base = index_base;
+        la.out = d_out;
+        la.out_idx = d_idx;
+        la.fb_count = fb;
+        la.fb_list = fb + 1;
+        const size_t sel_smem = static_cast<size_t>(NC) * 8;
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(select_large_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(sel_smem)));
+        {
+            ProfileScope ps(stream, "select_large_kernel");
+            select_large_kernel<<<static_cast<unsigned>(n), LK_THREADS, sel_smem, stream>>>(la);
+        }
+        KNN_LAUNCH_CHECK();
+    } else {
     switch (L.Kq) {
         case 4: launch_filter(filter_kernel<4>); break;
         case 8: launch_filter(filter_kernel<8>); break;
@@ -1263,8 +1717,9 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
                      h[4] / warps, h[0] / (warps * 32.0), h[1] / warps, h[2] / warps,
                      h[3] / (warps * 32.0), h[5] / warps / 1e3, h[6] / warps / 1e3, h[7] / warps / 1e3);
     }
+    }  // small k
 
-    // 3. exact re-rank
+    // 3. exact re-rank (small k; large k selected above)
     RerankArgs ra{};
     ra.Q = dQ;
     ra.R = dR;
@@ -1282,7 +1737,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ra.fb_count = fb;
     ra.fb_list = fb + 1;
     const size_t rr_smem = static_cast<size_t>(RR_WARPS) * rr_warp_bytes(S_max * L.Kq, k);
-    {
+    if (!large) {
         ProfileScope ps(stream, "rerank_kernel");
         rerank_kernel<<<static_cast<unsigned>((n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, rr_smem,
                         stream>>>(ra);
@@ -1315,7 +1770,11 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
                 dQ, d, dl, fails, gq);
         }
         KNN_LAUNCH_CHECK();
-        run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
+        if (large && !retry)  // a tail estimate of T0: once more from fresh seed tiles
+            run_tensor_path(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi,
+                            margin, true);
+        else
+            run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
         {
             const int64_t tot = static_cast<int64_t>(fails) * k;
             ProfileScope ps(stream, "fallback_scatter");

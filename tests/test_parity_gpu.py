@@ -159,11 +159,13 @@ def test_config_b_subsample(knn, oracle):
     check_invariants(t, m)
 
 
-def test_paths_are_bitwise_identical(knn, oracle):
-    """C3 analogue: exact / tensor / auto give bitwise-equal tables."""
+@pytest.mark.parametrize("k", [17, 150])
+def test_paths_are_bitwise_identical(knn, oracle, k):
+    """C3 analogue: exact / tensor / auto give bitwise-equal tables (k=17: the
+    running-bound tensor path; k=150: the large-k fixed-threshold path)."""
     R = oracle.uniform_f32(9000, 40, 11)
     Q = oracle.uniform_f32(1000, 40, 12)
-    tabs = [knn.bf_knn(Q, R, 17, config=cfg(knn, p)) for p in PATHS]
+    tabs = [knn.bf_knn(Q, R, k, config=cfg(knn, p)) for p in PATHS]
     for t in tabs[1:]:
         assert (t.index == tabs[0].index).all()
         assert (t.distance == tabs[0].distance).all()
