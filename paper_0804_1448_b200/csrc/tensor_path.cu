@@ -1000,7 +1000,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // logged {A, index} values, bitonic-sort them by A, A_(k) = k-th; certify
 // (>= k logged, no overflow, thresh(A_(k)) <= T0); exact FP32 keys of every
 // value <= thresh(A_(k)); bitonic sort by (key, index); top k.
-constexpr int LK_THREADS = 256;
+constexpr int LK_THREADS = 512;
 #ifndef KNN_DBG_LARGE
 #define KNN_DBG_LARGE 0
 #endif
@@ -1051,14 +1051,31 @@ __device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist
                 atomicAdd(hist + bin, static_cast<unsigned>(__popc(same)));
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0, b = 0;
-            for (; b < 256; ++b) {
-                if (acc + static_cast<int>(hist[b]) >= want) break;
-                acc += static_cast<int>(hist[b]);
+        if (threadIdx.x < 32) {  // warp 0: the bin holding rank `want` (8 bins per lane)
+            const int l = threadIdx.x;
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = hist[8 * l + j];
+                tot += c[j];
             }
-            scratch[0] = b;
-            scratch[1] = want - acc;
+            unsigned incl = tot;  // inclusive prefix over lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (l >= o) incl += y;
+            }
+            const unsigned excl = incl - tot;
+            if (excl < static_cast<unsigned>(want) && static_cast<unsigned>(want) <= incl) {
+                unsigned acc = excl;
+                int j = 0;
+                for (; j < 7; ++j) {
+                    if (acc + c[j] >= static_cast<unsigned>(want)) break;
+                    acc += c[j];
+                }
+                scratch[0] = 8 * l + j;
+                scratch[1] = want - static_cast<int>(acc);
+            }
         }
         __syncthreads();
         const unsigned b = static_cast<unsigned>(scratch[0]);
@@ -1135,7 +1152,7 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
             // compact the candidates (A <= tau) to the front, any order
             if (threadIdx.x == 0) s_cnt = 0;
             __syncthreads();
-            int mine[32];  // total <= NC <= 32 * LK_THREADS: a thread owns <= 32 entries
+            int mine[16];  // total <= NC <= 16 * LK_THREADS: a thread owns <= 16 entries
             int nm = 0;
             for (int e = threadIdx.x; e < total; e += blockDim.x)
                 if (sk[e] <= tau) mine[nm++] = si[e];
@@ -1676,7 +1693,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         la.S_max = S_max;
         int NC = 1;
         while (NC < 2 * margin * k) NC <<= 1;
-        NC = std::min(NC, 32 * LK_THREADS);
+        NC = std::min(NC, 16 * LK_THREADS);
         la.NC = NC;
         la.f = fa;
         la.raw_keys = raw_keys;

@@ -15,7 +15,7 @@ bool tensor_path_supported(int64_t n, int64_t m, int d, int k);
 // tiles before the exact path.
 void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
-                     float* d_out, int64_t* d_idx, int margin = 3, bool retry = false);
+                     float* d_out, int64_t* d_idx, int margin = 2, bool retry = false);
 
 // exact path on a subset of queries (certification fallback), defined in engine.cu
 void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
