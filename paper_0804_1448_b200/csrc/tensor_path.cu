@@ -54,7 +54,7 @@ constexpr int EPI_WARPS = 8;       // two sets of four (one warp per TMEM lane q
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 128 + EPI_THREADS;  // producer, MMA, TMEM-alloc, spare + epilogue
 constexpr int KEXTRA = 0;          // bound list K' >= k + KEXTRA
-constexpr int kLogGroups = 256;    // logged candidate groups per (query, CTA part)
+constexpr int kLogGroups = 256;    // minimum logged candidate groups per (query, CTA part)
 constexpr int kMaxLargeK = 1024;   // k > MAX_KQ: fixed-threshold filter + block selection
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
@@ -1520,7 +1520,14 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
     sz.take<float>(static_cast<size_t>(d) + 1);
     const bool large = k > MAX_KQ;
-    const int CG = large ? 0 : kLogGroups;
+    // group-log capacity: ~1.5x the expected number of running-bound records
+    // of a whole pair stream, k (1 + ln(groups / k)), at least 256
+    int CG = 0;
+    if (!large) {
+        const double recs = k * (1.0 + std::log(std::max(1.0, (m / 8.0) / k)));
+        CG = kLogGroups;
+        while (CG < 1.5 * recs && CG < 4096) CG *= 2;
+    }
     // large k: T0 ~ the (2k)-th smallest A; log room for twice that per part
     const int CV = large ? 2 * margin * k + 256 : 0;
     const int64_t np_list = large ? 0 : parts;
