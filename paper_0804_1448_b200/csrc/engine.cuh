@@ -49,6 +49,7 @@ struct DeviceContext {
     cudaStream_t stream = nullptr;
     DeviceArena arena;       // per-search scratch
     DeviceArena io;          // host-API staging of inputs / outputs
+    DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
     std::mutex mu;           // one search at a time per context
     int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
 };

@@ -1099,6 +1099,7 @@ struct LargeArgs {
     int64_t* out_idx;
     int* fb_count;
     int* fb_list;
+    int fb_offset;
 };
 
 __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
@@ -1166,7 +1167,7 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
     if (!ok) {
         if (threadIdx.x == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
-            a.fb_list[slot] = static_cast<int>(q);
+            a.fb_list[slot] = a.fb_offset + static_cast<int>(q);
             if (KNN_DBG_LARGE && slot < 8)
                 printf("[select_large] q=%lld total=%d k=%d NC=%d tau=%g T0=%g nc=%d\n",
                        static_cast<long long>(q), total, k, a.NC, tau, T0, nc);
@@ -1244,6 +1245,7 @@ struct RerankArgs {
     int64_t* out_idx;
     int* fb_count;
     int* fb_list;
+    int fb_offset;         // added to the recorded query index (deferred fallbacks)
 };
 
 constexpr int RR_WARPS = 4;
@@ -1360,7 +1362,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     if (!ok) {
         if (lane == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
-            a.fb_list[slot] = static_cast<int>(q);
+            a.fb_list[slot] = a.fb_offset + static_cast<int>(q);
         }
         return;
     }
@@ -1489,9 +1491,93 @@ bool tensor_path_supported(int64_t n, int64_t m, int d, int k) {
     return layout_for(d, k).stages >= 2;
 }
 
+size_t tensor_refs_bytes(int64_t m, int d) {
+    const Layout L = layout_for(d, 1);
+    const int64_t m_pad = (m + TILE - 1) / TILE * TILE;
+    Sizer sz;
+    sz.take<__half>(static_cast<size_t>(m_pad) * L.Kp);
+    sz.take<float>(static_cast<size_t>(m_pad));
+    sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
+    sz.take<float>(static_cast<size_t>(d) + 1);
+    return sz.used + 256;
+}
+
+// Reference side of the tensor path, independent of the queries: per-dimension
+// midrange centre and power-of-two scale of R, fp16 copy with the folded
+// squared norms, rounding radii.  (The centre/scale only shape the fp16
+// rounding: queries outside R's range round with their own, larger, delta and
+// the certificate (sec. 4 of DESIGN.md) accounts for it; a query whose
+// coordinates overflow fp16 yields no candidates and is recomputed exactly.)
+void tensor_prep_refs(cudaStream_t stream, const float* dR, int64_t m, int d, void* mem,
+                      TensorRefs& r) {
+    const Layout L = layout_for(d, 1);
+    r.dR = dR;
+    r.m = m;
+    r.d = d;
+    r.m_pad = (m + TILE - 1) / TILE * TILE;
+    Carver cv{static_cast<char*>(mem)};
+    r.Rh = cv.take<__half>(static_cast<size_t>(r.m_pad) * L.Kp);
+    r.rnorm = cv.take<float>(static_cast<size_t>(r.m_pad));
+    unsigned* mnmx = cv.take<unsigned>(2 * static_cast<size_t>(d) + 2);
+    r.mu = cv.take<float>(static_cast<size_t>(d) + 1);
+    r.scale = r.mu + d;
+    r.gmax = mnmx + 2 * d;
+    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx, 0xff, sizeof(unsigned) * d, stream));
+    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx + d, 0x00, sizeof(unsigned) * d, stream));
+    {
+        ProfileScope ps(stream, "prep_range_kernel");
+        const int vec = (d % 4 == 0) ? 4 : 1;
+        const int rpb = 256 / (d / vec);
+        const int64_t want = (m + rpb * 8 - 1) / (rpb * 8);  // >= 8 rows per thread
+        const unsigned grid =
+            static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * kSmCount)));
+        if (vec == 4)
+            range_kernel<4><<<grid, 256, 0, stream>>>(dR, m, d, mnmx, mnmx + d);
+        else
+            range_kernel<1><<<grid, 256, 0, stream>>>(dR, m, d, mnmx, mnmx + d);
+    }
+    KNN_LAUNCH_CHECK();
+    {
+        ProfileScope ps(stream, "prep_scale_kernel");
+        scale_kernel<<<1, 256, 0, stream>>>(mnmx, mnmx + d, d, L.Kp, r.mu, r.scale, r.gmax);
+    }
+    KNN_LAUNCH_CHECK();
+    PrepArgs pr{};
+    pr.d = d;
+    pr.Kp = L.Kp;
+    pr.norm_col = L.fold ? L.norm_col : -1;
+    pr.mu = r.mu;
+    pr.scale = r.scale;
+    pr.gmax = r.gmax;
+    pr.X = dR;
+    pr.rows = m;
+    pr.rows_pad = r.m_pad;
+    pr.Xh = r.Rh;
+    pr.norm = r.rnorm;
+    {
+        ProfileScope ps(stream, "prep_convert_refs");
+        convert_kernel<false>
+            <<<static_cast<unsigned>(std::min<int64_t>((r.m_pad + 7) / 8, 8 * kSmCount)), 256, 0,
+               stream>>>(pr);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
 void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
-                     float* d_out, int64_t* d_idx, int margin, bool retry) {
+                     float* d_out, int64_t* d_idx) {
+    ctx.refs.reserve(tensor_refs_bytes(m, d));
+    TensorRefs r;
+    tensor_prep_refs(stream, dR, m, d, ctx.refs.base(), r);
+    tensor_search(ctx, stream, r, dQ, n, k, raw_keys, index_base, d_out, d_idx);
+}
+
+void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
+                   const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
+                   float* d_out, int64_t* d_idx, const FallbackSink* sink, int margin, bool retry) {
+    const float* dR = refs.dR;
+    const int64_t m = refs.m;
+    const int d = refs.d;
     const Layout L = layout_for(d, k);
     const int pairs = static_cast<int>((n + 2 * TILE - 1) / (2 * TILE));
     const int qtiles = 2 * pairs;  // the last tile of the last pair may be all padding
@@ -1514,11 +1600,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
 
     Sizer sz;
     sz.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
-    sz.take<__half>(static_cast<size_t>(m_pad) * L.Kp);
-    sz.take<float>(static_cast<size_t>(m_pad));
     sz.take<float4>(static_cast<size_t>(n_pad));
-    sz.take<unsigned>(2 * static_cast<size_t>(d) + 2);
-    sz.take<float>(static_cast<size_t>(d) + 1);
     const bool large = k > MAX_KQ;
     // group-log capacity: ~1.5x the expected number of running-bound records
     // of a whole pair stream, k (1 + ln(groups / k)), at least 256
@@ -1543,11 +1625,9 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
-    __half* Rh = cv.take<__half>(static_cast<size_t>(m_pad) * L.Kp);
-    float* rnorm = cv.take<float>(static_cast<size_t>(m_pad));
+    __half* Rh = refs.Rh;
+    const float* rnorm = refs.rnorm;
     float4* qconst = cv.take<float4>(static_cast<size_t>(n_pad));
-    unsigned* mnmx = cv.take<unsigned>(2 * static_cast<size_t>(d) + 2);
-    float* mu = cv.take<float>(static_cast<size_t>(d) + 1);
     float* part_A = cv.take<float>(static_cast<size_t>(np_list) * L.Kq * TILE);
     int* part_cnt = cv.take<int>(static_cast<size_t>(parts) * TILE);
     int* log_n = cv.take<int>(static_cast<size_t>(parts) * TILE);
@@ -1557,57 +1637,20 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
     float* t0 = cv.take<float>(large ? static_cast<size_t>(n_pad) : 0);
     float2* vlog = cv.take<float2>(static_cast<size_t>(parts) * TILE * CV);
-    unsigned* gmax = mnmx + 2 * d;
-    float* scale = mu + d;
+    const unsigned* gmax = refs.gmax;
 
-    // 1. prep
-    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx, 0xff, sizeof(unsigned) * d, stream));
-    KNN_CUDA_CHECK(cudaMemsetAsync(mnmx + d, 0x00, sizeof(unsigned) * d, stream));
+    // 1. per-search state and the query-side prep
     KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(log_n, 0, sizeof(int) * parts * TILE, stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
     KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
-    {
-        ProfileScope ps(stream, "prep_range_kernel");
-        auto range = [&](const float* X, int64_t rows) {
-            const int vec = (d % 4 == 0) ? 4 : 1;
-            const int rpb = 256 / (d / vec);
-            const int64_t want = (rows + rpb * 8 - 1) / (rpb * 8);  // >= 8 rows per thread
-            const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-                1, std::min<int64_t>(want, 4 * kSmCount)));
-            if (vec == 4)
-                range_kernel<4><<<grid, 256, 0, stream>>>(X, rows, d, mnmx, mnmx + d);
-            else
-                range_kernel<1><<<grid, 256, 0, stream>>>(X, rows, d, mnmx, mnmx + d);
-        };
-        range(dR, m);
-        range(dQ, n);
-    }
-    KNN_LAUNCH_CHECK();
-    note_launch();
-    {
-        ProfileScope ps(stream, "prep_scale_kernel");
-        scale_kernel<<<1, 256, 0, stream>>>(mnmx, mnmx + d, d, L.Kp, mu, scale, gmax);
-    }
-    KNN_LAUNCH_CHECK();
     PrepArgs pr{};
     pr.d = d;
     pr.Kp = L.Kp;
     pr.norm_col = L.fold ? L.norm_col : -1;
-    pr.mu = mu;
-    pr.scale = scale;
-    pr.gmax = gmax;
-    pr.X = dR;
-    pr.rows = m;
-    pr.rows_pad = m_pad;
-    pr.Xh = Rh;
-    pr.norm = rnorm;
-    {
-        ProfileScope ps(stream, "prep_convert_refs");
-        convert_kernel<false><<<static_cast<unsigned>(std::min<int64_t>((m_pad + 7) / 8, 8 * kSmCount)),
-                                256, 0, stream>>>(pr);
-    }
-    KNN_LAUNCH_CHECK();
+    pr.mu = refs.mu;
+    pr.scale = refs.scale;
+    pr.gmax = nullptr;
     pr.X = dQ;
     pr.rows = n;
     pr.rows_pad = n_pad;
@@ -1707,8 +1750,9 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         la.index_base = index_base;
         la.out = d_out;
         la.out_idx = d_idx;
-        la.fb_count = fb;
-        la.fb_list = fb + 1;
+        la.fb_count = sink ? sink->count : fb;
+        la.fb_list = sink ? sink->list : fb + 1;
+        la.fb_offset = sink ? sink->offset : 0;
         const size_t sel_smem = static_cast<size_t>(NC) * 8;
         KNN_CUDA_CHECK(cudaFuncSetAttribute(select_large_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1758,8 +1802,9 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     ra.index_base = index_base;
     ra.out = d_out;
     ra.out_idx = d_idx;
-    ra.fb_count = fb;
-    ra.fb_list = fb + 1;
+    ra.fb_count = sink ? sink->count : fb;
+    ra.fb_list = sink ? sink->list : fb + 1;
+    ra.fb_offset = sink ? sink->offset : 0;
     const size_t rr_smem = static_cast<size_t>(RR_WARPS) * rr_warp_bytes(S_max * L.Kq, k);
     if (!large) {
         ProfileScope ps(stream, "rerank_kernel");
@@ -1768,7 +1813,9 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     }
     KNN_LAUNCH_CHECK();
 
-    // 4. certification fallback (exact kernel on the failed queries)
+    // 4. certification fallback (exact kernel on the failed queries), unless
+    //    the caller collects them across several searches
+    if (sink) return;
     int fails = 0;
     KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
     KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
@@ -1795,8 +1842,8 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         }
         KNN_LAUNCH_CHECK();
         if (large && !retry)  // a tail estimate of T0: once more from fresh seed tiles
-            run_tensor_path(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi,
-                            margin, true);
+            tensor_search(ctx, stream, refs, gq, fails, k, raw_keys, index_base, od, oi, nullptr,
+                          margin, true);
         else
             run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
         {
