@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "engine.cuh"
 #include "exact_kernel.cuh"
+#include "tensor_path.cuh"
 
 namespace knnb200 {
 
@@ -72,11 +73,12 @@ void check_point_set(const float* data, int64_t n, int64_t d, bool check_values)
 // Device-side PointSet value check (point_set.hpp:27-31): first index of a
 // non-finite coordinate (atomicMin), so the host API validates a device copy
 // in microseconds instead of scanning n*d values on one host core.
-__global__ void finite_scan_kernel(const float* X, int64_t count, unsigned long long* first) {
+__global__ void finite_scan_kernel(const float* X, int64_t count, unsigned long long* first,
+                                   int64_t base = 0) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
          i += stride) {
-        if (!isfinite(__ldg(X + i))) atomicMin(first, static_cast<unsigned long long>(i));
+        if (!isfinite(__ldg(X + i))) atomicMin(first, static_cast<unsigned long long>(base + i));
     }
 }
 
@@ -178,10 +180,180 @@ struct knn_b200_index {
     int d = 0;
     int64_t base = 0;
     std::mutex mu;
+    // tensor path: the reference set prepared once (fp16 copy, norms, radii)
+    // on the first tensor search, reused by every later search (the KdTree
+    // build/search split, kdtree.hpp:21,70-72)
+    knnb200::TensorRefs tref;
+    void* tref_mem = nullptr;
     ~knn_b200_index() {
         if (owned && dR) cudaFree(const_cast<float*>(dR));
+        if (tref_mem) cudaFree(tref_mem);
     }
 };
+
+namespace knnb200 {
+namespace {
+const TensorRefs* index_refs(knn_b200_index* h, int64_t n, int k, int metric, int path,
+                             cudaStream_t s) {
+    if (plan_search(n, h->m, h->d, k, metric, path).path != 2) return nullptr;
+    if (!h->tref_mem) {
+        KNN_CUDA_CHECK(cudaMalloc(&h->tref_mem, tensor_refs_bytes(h->m, h->d)));
+        tensor_prep_refs(s, h->dR, h->m, h->d, h->tref_mem, h->tref);
+    }
+    return &h->tref;
+}
+}  // namespace
+}  // namespace knnb200
+
+namespace knnb200 {
+namespace {
+
+// queries per pipeline stage (multiple of 256): large enough that a chunk's
+// search runs near full efficiency (one chunk per ~128 query-tile pairs)
+constexpr int64_t kPipeChunk = 32768;
+
+unsigned scan_grid(int64_t count) {
+    return static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 1184));
+}
+
+// One-shot host search, staged: H2D of both sets, device value check, search, D2H.
+void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r, int64_t m,
+                   int dq, int dr, int k, int metric, int path, int raw_keys, bool host_values,
+                   float* out_dist, int64_t* out_idx) {
+    cudaStream_t s = ctx.stream;
+    Sizer sz;
+    sz.take<float>(static_cast<size_t>(n) * dq);
+    sz.take<float>(static_cast<size_t>(m) * dr);
+    sz.take<float>(static_cast<size_t>(n) * k);
+    sz.take<int64_t>(static_cast<size_t>(n) * k);
+    sz.take<unsigned long long>(2);
+    ctx.io.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.io.base())};
+    float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
+    float* dR = cv.take<float>(static_cast<size_t>(m) * dr);
+    float* dO = cv.take<float>(static_cast<size_t>(n) * k);
+    int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
+    unsigned long long* dbad = cv.take<unsigned long long>(2);
+    KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, q, sizeof(float) * n * dq, cudaMemcpyHostToDevice, s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * dr, cudaMemcpyHostToDevice, s));
+    if (!host_values) {
+        KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
+        finite_scan_kernel<<<scan_grid(n * dq), 256, 0, s>>>(dQ, n * dq, dbad);
+        KNN_LAUNCH_CHECK();
+        finite_scan_kernel<<<scan_grid(m * dr), 256, 0, s>>>(dR, m * dr, dbad + 1);
+        KNN_LAUNCH_CHECK();
+        unsigned long long bad[2];
+        KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+        KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (bad[0] != ~0ull) throw_non_finite(bad[0], dq);
+        if (bad[1] != ~0ull) throw_non_finite(bad[1], dr);
+    }
+    search_device(ctx, s, dQ, n, dR, m, dq, k, metric, path, raw_keys, 0, dO, dI);
+    KNN_CUDA_CHECK(cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(out_idx, dI, sizeof(int64_t) * n * k, cudaMemcpyDeviceToHost, s));
+    KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// One-shot host search on the tensor path, pipelined over query chunks: the
+// reference set is copied and prepared once, then chunk c's H2D (copy stream)
+// overlaps chunk c-1's search (compute stream), whose D2H overlaps chunk c's
+// search.  Coordinates are validated on the device and checked before any
+// result is returned; certification fallbacks of all chunks are collected and
+// resolved once at the end.
+void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float* r, int64_t m,
+                      int d, int k, int raw_keys, float* out_dist, int64_t* out_idx) {
+    cudaStream_t s = ctx.stream, cs = ctx.copy_stream;
+    Sizer sz;
+    sz.take<float>(static_cast<size_t>(n) * d);
+    sz.take<float>(static_cast<size_t>(m) * d);
+    sz.take<float>(static_cast<size_t>(n) * k);
+    sz.take<int64_t>(static_cast<size_t>(n) * k);
+    sz.take<unsigned long long>(2);
+    sz.take<int>(static_cast<size_t>(n) + 1);
+    ctx.io.reserve(sz.used + 256);
+    ctx.refs.reserve(tensor_refs_bytes(m, d));
+    Carver cv{static_cast<char*>(ctx.io.base())};
+    float* dQ = cv.take<float>(static_cast<size_t>(n) * d);
+    float* dR = cv.take<float>(static_cast<size_t>(m) * d);
+    float* dO = cv.take<float>(static_cast<size_t>(n) * k);
+    int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
+    unsigned long long* dbad = cv.take<unsigned long long>(2);
+    int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
+    KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
+    KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * d, cudaMemcpyHostToDevice, s));
+    finite_scan_kernel<<<scan_grid(m * d), 256, 0, s>>>(dR, m * d, dbad + 1);
+    KNN_LAUNCH_CHECK();
+    TensorRefs refs;
+    tensor_prep_refs(s, dR, m, d, ctx.refs.base(), refs);
+    // the copy stream may only start once the events of the previous call are done
+    KNN_CUDA_CHECK(cudaEventRecord(ctx.ev[0], s));
+    KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx.ev[0], 0));
+    const int64_t chunks = (n + kPipeChunk - 1) / kPipeChunk;
+    FallbackSink sink{fb, fb + 1, 0};
+    for (int64_t c = 0; c < chunks; ++c) {
+        const int64_t q0 = c * kPipeChunk, nq = std::min(kPipeChunk, n - q0);
+        cudaEvent_t in = ctx.ev[1 + 2 * (c % 7)], done = ctx.ev[2 + 2 * (c % 7)];
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dQ + q0 * d, q + q0 * d, sizeof(float) * nq * d,
+                                       cudaMemcpyHostToDevice, cs));
+        KNN_CUDA_CHECK(cudaEventRecord(in, cs));
+        KNN_CUDA_CHECK(cudaStreamWaitEvent(s, in, 0));
+        finite_scan_kernel<<<scan_grid(nq * d), 256, 0, s>>>(dQ + q0 * d, nq * d, dbad, q0 * d);
+        KNN_LAUNCH_CHECK();
+        sink.offset = static_cast<int>(q0);
+        tensor_search(ctx, s, refs, dQ + q0 * d, nq, k, raw_keys, 0, dO + q0 * k, dI + q0 * k,
+                      &sink);
+        KNN_CUDA_CHECK(cudaEventRecord(done, s));
+        KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, done, 0));
+        KNN_CUDA_CHECK(cudaMemcpyAsync(out_dist + q0 * k, dO + q0 * k, sizeof(float) * nq * k,
+                                       cudaMemcpyDeviceToHost, cs));
+        KNN_CUDA_CHECK(cudaMemcpyAsync(out_idx + q0 * k, dI + q0 * k, sizeof(int64_t) * nq * k,
+                                       cudaMemcpyDeviceToHost, cs));
+    }
+    unsigned long long bad[2];
+    int fails = 0;
+    KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, s));
+    KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    KNN_CUDA_CHECK(cudaStreamSynchronize(cs));
+    if (bad[0] != ~0ull) throw_non_finite(bad[0], d);
+    if (bad[1] != ~0ull) throw_non_finite(bad[1], d);
+    ctx.last_fallbacks = fails;
+    if (fails == 0) return;
+    // uncertified queries: the full dispatch (large-k retry, exact) on their rows
+    std::vector<int> list(static_cast<size_t>(fails));
+    KNN_CUDA_CHECK(cudaMemcpy(list.data(), fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToHost));
+    std::vector<float> gq(static_cast<size_t>(fails) * d);
+    for (int i = 0; i < fails; ++i)
+        std::memcpy(gq.data() + static_cast<size_t>(i) * d, q + static_cast<int64_t>(list[i]) * d,
+                    sizeof(float) * d);
+    std::vector<float> sd(static_cast<size_t>(fails) * k);
+    std::vector<int64_t> si(static_cast<size_t>(fails) * k);
+    float* gdq = nullptr;
+    float* gdo = nullptr;
+    int64_t* gdi = nullptr;
+    KNN_CUDA_CHECK(cudaMalloc(&gdq, sizeof(float) * gq.size()));
+    KNN_CUDA_CHECK(cudaMalloc(&gdo, sizeof(float) * sd.size()));
+    KNN_CUDA_CHECK(cudaMalloc(&gdi, sizeof(int64_t) * si.size()));
+    KNN_CUDA_CHECK(cudaMemcpy(gdq, gq.data(), sizeof(float) * gq.size(), cudaMemcpyHostToDevice));
+    search_device(ctx, s, gdq, fails, dR, m, d, k, kL2, 2, raw_keys, 0, gdo, gdi);
+    KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    KNN_CUDA_CHECK(cudaMemcpy(sd.data(), gdo, sizeof(float) * sd.size(), cudaMemcpyDeviceToHost));
+    KNN_CUDA_CHECK(cudaMemcpy(si.data(), gdi, sizeof(int64_t) * si.size(), cudaMemcpyDeviceToHost));
+    cudaFree(gdq);
+    cudaFree(gdo);
+    cudaFree(gdi);
+    for (int i = 0; i < fails; ++i) {
+        std::memcpy(out_dist + static_cast<int64_t>(list[i]) * k, sd.data() + static_cast<size_t>(i) * k,
+                    sizeof(float) * k);
+        std::memcpy(out_idx + static_cast<int64_t>(list[i]) * k, si.data() + static_cast<size_t>(i) * k,
+                    sizeof(int64_t) * k);
+    }
+    ctx.last_fallbacks = fails;
+}
+
+}  // namespace
+}  // namespace knnb200
 
 extern "C" {
 
@@ -240,42 +412,12 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         DeviceContext& ctx = context_for(o.device);
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
-        cudaStream_t s = ctx.stream;
-        Sizer sz;
-        sz.take<float>(static_cast<size_t>(n) * dq);
-        sz.take<float>(static_cast<size_t>(m) * dr);
-        sz.take<float>(static_cast<size_t>(n) * k);
-        sz.take<int64_t>(static_cast<size_t>(n) * k);
-        sz.take<unsigned long long>(2);
-        ctx.io.reserve(sz.used + 256);
-        Carver cv{static_cast<char*>(ctx.io.base())};
-        float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
-        float* dR = cv.take<float>(static_cast<size_t>(m) * dr);
-        float* dO = cv.take<float>(static_cast<size_t>(n) * k);
-        int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
-        unsigned long long* dbad = cv.take<unsigned long long>(2);
-        KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, q, sizeof(float) * n * dq, cudaMemcpyHostToDevice, s));
-        KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * dr, cudaMemcpyHostToDevice, s));
-        if (!host_values) {
-            KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
-            const unsigned gq = static_cast<unsigned>(std::min<int64_t>((n * dq + 255) / 256, 1184));
-            const unsigned gr = static_cast<unsigned>(std::min<int64_t>((m * dr + 255) / 256, 1184));
-            finite_scan_kernel<<<gq, 256, 0, s>>>(dQ, n * dq, dbad);
-            KNN_LAUNCH_CHECK();
-            finite_scan_kernel<<<gr, 256, 0, s>>>(dR, m * dr, dbad + 1);
-            KNN_LAUNCH_CHECK();
-            unsigned long long bad[2];
-            KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));
-            KNN_CUDA_CHECK(cudaStreamSynchronize(s));
-            if (bad[0] != ~0ull) throw_non_finite(bad[0], dq);
-            if (bad[1] != ~0ull) throw_non_finite(bad[1], dr);
-        }
-        search_device(ctx, s, dQ, n, dR, m, dq, k, kernel_metric, o.path, o.raw_keys, 0, dO, dI);
-        KNN_CUDA_CHECK(
-            cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
-        KNN_CUDA_CHECK(
-            cudaMemcpyAsync(out_idx, dI, sizeof(int64_t) * n * k, cudaMemcpyDeviceToHost, s));
-        KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (plan_search(n, m, dq, k, kernel_metric, o.path).path == 2 && !host_values &&
+            n >= 2 * kPipeChunk)
+            search_pipelined(ctx, q, n, r, m, dq, k, o.raw_keys, out_dist, out_idx);
+        else
+            search_staged(ctx, q, n, r, m, dq, dr, k, kernel_metric, o.path, o.raw_keys, host_values,
+                          out_dist, out_idx);
         if (distance_evals)
             *distance_evals = o.count_distance_evals ? static_cast<uint64_t>(n) * m : 0;
     });
@@ -384,7 +526,8 @@ knn_b200_status knn_b200_index_search(knn_b200_index* index, const float* querie
         KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, queries, sizeof(float) * n * index->d,
                                        cudaMemcpyHostToDevice, s));
         search_device(ctx, s, dQ, n, index->dR, index->m, index->d, k, metric, o.path,
-                      o.raw_keys, index->base, dO, dI);
+                      o.raw_keys, index->base, dO, dI,
+                      index_refs(index, n, k, metric, o.path, s));
         KNN_CUDA_CHECK(
             cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
         KNN_CUDA_CHECK(
@@ -411,7 +554,8 @@ knn_b200_status knn_b200_index_search_device(knn_b200_index* index, const float*
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
         search_device(ctx, s, d_queries, n, index->dR, index->m, index->d, k, metric, o.path,
-                      o.raw_keys, index->base, d_out_dist, d_out_idx);
+                      o.raw_keys, index->base, d_out_dist, d_out_idx,
+                      index_refs(index, n, k, metric, o.path, s));
         if (!o.stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }

@@ -49,6 +49,8 @@ DeviceContext& context_for(int device) {
         slot->device = device;
         KNN_CUDA_CHECK(cudaSetDevice(device));
         KNN_CUDA_CHECK(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+        KNN_CUDA_CHECK(cudaStreamCreateWithFlags(&slot->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : slot->ev) KNN_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return *slot;
 }
@@ -136,10 +138,14 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
 
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                    const float* dR, int64_t m, int d, int k, int metric, int path,
-                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx) {
+                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx,
+                   const TensorRefs* refs) {
     const SearchPlan plan = plan_search(n, m, d, k, metric, path);
     if (plan.path == 2) {
-        run_tensor_path(ctx, stream, dQ, n, dR, m, d, k, raw_keys, index_base, d_out, d_idx);
+        if (refs)  // reference set already prepared (index handle)
+            tensor_search(ctx, stream, *refs, dQ, n, k, raw_keys, index_base, d_out, d_idx);
+        else
+            run_tensor_path(ctx, stream, dQ, n, dR, m, d, k, raw_keys, index_base, d_out, d_idx);
         return;
     }
     run_exact(ctx, stream, dQ, n, dR, m, d, k, metric, plan.splits, raw_keys, index_base, d_out,

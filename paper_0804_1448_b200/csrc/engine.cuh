@@ -47,6 +47,8 @@ struct Sizer {
 struct DeviceContext {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // host API: H2D / D2H overlapped with compute
+    cudaEvent_t ev[16] = {};              // host API pipeline events
     DeviceArena arena;       // per-search scratch
     DeviceArena io;          // host-API staging of inputs / outputs
     DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
@@ -61,11 +63,15 @@ struct SearchPlan {
     int splits;     // reference-axis splits for the exact path
 };
 
+struct TensorRefs;
+
 // Core device search.  All pointers are device pointers.  Output: finalized
 // distances (or raw keys when raw_keys) and global indices (index_base + j).
+// refs: the tensor path's prepared reference set (index handles), optional.
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                    const float* dR, int64_t m, int d, int k, int metric, int path,
-                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx);
+                   int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx,
+                   const TensorRefs* refs = nullptr);
 
 SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path);
 

@@ -293,3 +293,28 @@ def test_non_finite_detected_on_device(knn, oracle):
     t = knn.bf_knn(Q, R, 5)
     ri, rd = oracle.knn(Q[:50], R, 5)
     assert compare(t.index[:50], t.distance[:50], ri, rd, Q[:50], R, oracle=oracle).ok
+
+
+def test_pipelined_host_search(knn, oracle):
+    """n >= 2 pipeline chunks: the one-shot host API overlaps query H2D / D2H
+    with the search.  Results, device-side value checks and the deferred
+    certification fallbacks behave as in the staged path."""
+    n, m, d, k = 70000, 3000, 24, 10
+    R = oracle.uniform_f32(m, d, 51)
+    Q = oracle.uniform_f32(n, d, 52)
+    t = knn.bf_knn(Q, R, k)
+    te = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (t.index == te.index).all() and (t.distance == te.distance).all()
+    Qb = Q.copy()
+    Qb[53333, 5] = np.nan
+    with pytest.raises(ValueError, match=r"^PointSet: non-finite coordinate at point 53333, dimension 5$"):
+        knn.bf_knn(Qb, R, k)
+    # a tie-saturated block of queries: uncertified, resolved after the pipeline
+    Rd = R.copy()
+    Rd[: 2000] = Rd[0]
+    Qd = Q.copy()
+    Qd[40000:40100] = Rd[0]
+    td = knn.bf_knn(Qd, Rd, k)
+    assert knn.last_fallback_count() > 0
+    tde = knn.bf_knn(Qd, Rd, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (td.index == tde.index).all() and (td.distance == tde.distance).all()
