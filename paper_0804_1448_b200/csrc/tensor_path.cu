@@ -1284,23 +1284,28 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     const int row = static_cast<int>(q % TILE);
     const int64_t p0 = static_cast<int64_t>(qt) * parts;
 
+    // Every step below issues its loads for the whole query at once (one
+    // memory round trip per step): the kernel is latency-bound per warp.
     int cnt = 0, nlog = 0;
     if (lane < parts) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
         nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
-    int incl = cnt;  // inclusive prefix of the list lengths over parts
+    const Consts qc = load_consts(a.f, q);
+    // 0. all bound lists, compacted: list p's entries go to [excl_p, excl_p + cnt_p)
+    int cincl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+        if (lane >= o) cincl += y;
     }
-    const int L = __shfl_sync(0xffffffffu, incl, 31);
-    const int excl = incl - cnt;
-    for (int p = 0; p < parts; ++p) {
-        const int cp = __shfl_sync(0xffffffffu, cnt, p);
-        const int ep = __shfl_sync(0xffffffffu, excl, p);
-        for (int e = lane; e < cp; e += 32) sv[ep + e] = a.f.part_A[((p0 + p) * Kq + e) * TILE + row];
+    const int L = __shfl_sync(0xffffffffu, cincl, 31);
+    for (int x0 = 0; x0 < span; x0 += 32) {
+        const int x = x0 + lane;
+        const int p = x / Kq, e = x - p * Kq;
+        const int cp = __shfl_sync(0xffffffffu, cnt, p & 31);
+        const int ep = __shfl_sync(0xffffffffu, cincl, p & 31) - cp;
+        if (x < span && e < cp) sv[ep + e] = a.f.part_A[((p0 + p) * Kq + e) * TILE + row];
     }
     __syncwarp();
 
@@ -1319,45 +1324,73 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
     }
-    const Consts qc = load_consts(a.f, q);
     const float tau = thresh(B, qc);
 
     // 2. certificate
     bool ok = __all_sync(0xffffffffu, nlog <= a.f.CG) && isfinite(tau);
 
-    // 3. candidates: logged values <= tau
+    // 3. candidates: logged values <= tau.  Heads of every logged group of
+    //    every part (flattened over parts), then the values of the groups whose
+    //    minimum is inside tau, then their values <= tau.
     int nc = 0;
     if (ok) {
-        for (int p = 0; p < parts; ++p) {
-            const int np = __shfl_sync(0xffffffffu, nlog, p);
-            const int64_t lq = ((p0 + p) * TILE + row) * a.f.CG;
-            for (int g0 = 0; g0 < np; g0 += 32) {
-                const int g = g0 + lane;
-                // group heads first (8 B each); the 8 values only where the
-                // group minimum is inside tau
-                const int2 hd = g < np ? a.f.log_h[lq + g] : make_int2(__float_as_int(kInf), 0);
-                const bool in = __int_as_float(hd.x) <= tau;
-                if (!__any_sync(0xffffffffu, in)) continue;
-                float w[8];
+        int incl = nlog;  // inclusive prefix of the log lengths over parts
 #pragma unroll
-                for (int e = 0; e < 8; ++e) w[e] = kInf;
-                if (in) {
-                    const float4 u = a.f.log_v[2 * (lq + g)], v = a.f.log_v[2 * (lq + g) + 1];
-                    w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
-                    w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
-                }
-                const int c0 = hd.y;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const bool c = w[e] <= tau;
-                    const unsigned bal = __ballot_sync(0xffffffffu, c);
-                    const int pos = nc + __popc(bal & ((1u << lane) - 1u));
-                    if (c && pos < RR_CAND) ci[pos] = c0 + e;
-                    nc += __popc(bal);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
+        int ng = 0;
+        for (int t0 = 0; t0 < total; t0 += 32) {
+            const int t = t0 + lane;
+            int p = 0, before = 0;  // part holding flattened group t, groups before it
+            for (int pp = 0; pp < parts; ++pp) {
+                const int ip = __shfl_sync(0xffffffffu, incl, pp);
+                if (t >= ip) {
+                    p = pp + 1;
+                    before = ip;
                 }
             }
+            int slot = -1;
+            bool in = false;
+            if (t < total) {
+                slot = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG + (t - before));
+                in = __int_as_float(a.f.log_h[slot].x) <= tau;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, in);
+            const int pos = ng + __popc(bal & ((1u << lane) - 1u));
+            if (in && pos < RR_CAND) gl[pos] = slot;
+            ng += __popc(bal);
         }
-        ok = nc <= RR_CAND && nc >= k;  // heavy ties beyond the fast path: exact kernel
+        ok = ng <= RR_CAND;
+        __syncwarp();
+        for (int j0 = 0; ok && j0 < ng; j0 += 32) {
+            const int j = j0 + lane;
+            float w[8];
+            int c0 = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w[e] = kInf;
+            if (j < ng) {
+                const int slot = gl[j];
+                const float4 u = a.f.log_v[2 * static_cast<int64_t>(slot)],
+                             v = a.f.log_v[2 * static_cast<int64_t>(slot) + 1];
+                w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+                w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
+                c0 = a.f.log_h[slot].y;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool c = w[e] <= tau;
+                const unsigned bal = __ballot_sync(0xffffffffu, c);
+                const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+                if (c && pos < RR_CAND) ci[pos] = c0 + e;
+                nc += __popc(bal);
+            }
+        }
+        ok = ok && nc <= RR_CAND && nc >= k;  // heavy ties beyond the fast path: exact kernel
     }
     if (!ok) {
         if (lane == 0) {
@@ -1376,7 +1409,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         if ((a.d & 3) == 0) {
             const float4* q4 = reinterpret_cast<const float4*>(qrow);
             const float4* r4 = reinterpret_cast<const float4*>(rrow);
-#pragma unroll 4
+#pragma unroll 8
             for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
                 const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
                 acc = key_step<kL2>(acc, u.x, w.x);
@@ -1403,7 +1436,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         }
     }
     __syncwarp();
-    if (!a.raw_keys) finalize_list(fk, fi, k, kL2, lane);
+    if (!a.raw_keys) finalize_list_runs(fk, fi, k, lane);
     for (int t = lane; t < k; t += 32) {
         a.out[q * k + t] = fk[t];
         a.out_idx[q * k + t] = a.index_base + fi[t];

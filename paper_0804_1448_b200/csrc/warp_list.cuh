@@ -146,4 +146,28 @@ __device__ void finalize_list(float* key, IdxT* idx, int k, int metric, int lane
     __syncwarp();
 }
 
+// finalize_list for L2 with the fix-up spread over the warp: keys were
+// ascending, so after sqrt every run of equal distances is contiguous; the lane
+// owning a run's first slot insertion-sorts the run's indices.
+template <typename IdxT>
+__device__ void finalize_list_runs(float* key, IdxT* idx, int k, int lane) {
+    for (int t = lane; t < k; t += 32) key[t] = __fsqrt_rn(key[t]);
+    __syncwarp();
+    for (int t = lane; t < k; t += 32) {
+        if (t > 0 && key[t - 1] == key[t]) continue;
+        int e = t + 1;
+        while (e < k && key[e] == key[t]) ++e;
+        for (int x = t + 1; x < e; ++x) {
+            const IdxT j = idx[x];
+            int u = x;
+            while (u > t && idx[u - 1] > j) {
+                idx[u] = idx[u - 1];
+                --u;
+            }
+            idx[u] = j;
+        }
+    }
+    __syncwarp();
+}
+
 }  // namespace knnb200
