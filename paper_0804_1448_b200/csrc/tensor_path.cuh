@@ -47,7 +47,7 @@ struct FallbackSink {
 void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
                    const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
                    float* d_out, int64_t* d_idx, const FallbackSink* sink = nullptr,
-                   int margin = 2, bool retry = false);
+                   int margin = 3, bool retry = false);
 
 // exact path on a subset of queries (certification fallback), defined in engine.cu
 void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
