@@ -208,10 +208,19 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
         const bool real = row < a.rows;
         double h2 = 0.0, e2 = 0.0;
         __half* out = a.Xh + row * a.Kp;
-        for (int c = lane; c < a.Kp; c += 32) {
+        float xv[5];  // this lane's coordinates, all loads in flight at once (Kp <= 160)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const int c = lane + 32 * j;
+            xv[j] = (real && c < a.d) ? __ldg(a.X + row * a.d + c) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const int c = lane + 32 * j;
+            if (c >= a.Kp) break;
             __half h = __float2half_rn(0.f);
             if (real && c < a.d) {
-                const float t = __fsub_rn(__ldg(a.X + row * a.d + c), a.mu[c]) * s;
+                const float t = __fsub_rn(xv[j], a.mu[c]) * s;
                 h = __float2half_rn(t);
                 const double hv = static_cast<double>(__half2float(h));
                 // fp16 rounding + the fp32 subtraction's rounding (<= 2^-24 |t|, doubled)
