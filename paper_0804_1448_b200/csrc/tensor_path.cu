@@ -87,6 +87,8 @@ struct PrepArgs {
     float* norm;        // refs, no-fold: ||r~||^2 per row (+inf padding)
     float4* qconst;     // queries: {nq, delta_q, ||q~||, 0}
     unsigned* gmax;     // refs: [0] max delta_r bits, [1] max ||r~|| bits
+    unsigned* tinit;    // queries: per-row cross-CTA bound, set to "none" (0xffffffff)
+    int* zero;          // queries: a counter cleared by block 0 (fallback count)
 };
 
 // ordered-uint encoding of floats for atomicMin/Max over signed values
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const float s = *a.scale;
+    if (QUERY && a.zero && blockIdx.x == 0 && threadIdx.x == 0) *a.zero = 0;
     // reference sets: running maxima of the rounding radius and of ||r~||,
     // reduced per block (one global atomic per block, not per row)
     float dmax = 0.f, nmax = 0.f;
@@ -243,6 +246,7 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
                 if (a.norm_col >= 0)
                     for (int j = 0; j < 3; ++j) out[a.norm_col + j] = __float2half_rn(1.f);
                 a.qconst[row] = make_float4(static_cast<float>(h2), delta, xn, 0.f);
+                if (a.tinit) a.tinit[row] = 0xffffffffu;
             } else if (a.norm_col >= 0) {
                 if (real) {
                     const __half p1 = __double2half(h2);
@@ -1126,8 +1130,12 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
     if (threadIdx.x == 0) {
         int off = 0;
         bool over = false;
+        const int pair = qt >> 1;  // slots written: one per CTA touching the pair
+        const int nslots = first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles + a.f.rtiles - 1,
+                                        a.f.U, a.f.G) -
+                           first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles, a.f.U, a.f.G) + 1;
         for (int p = 0; p < a.S_max; ++p) {
-            const int np = a.f.log_n[(p0 + p) * TILE + row];
+            const int np = p < nslots ? a.f.log_n[(p0 + p) * TILE + row] : 0;
             over |= np > a.f.CV;
             s_off[p] = off;
             off += min(np, a.f.CV);
@@ -1295,8 +1303,13 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
 
     // Every step below issues its loads for the whole query at once (one
     // memory round trip per step): the kernel is latency-bound per warp.
+    // part slots written for this pair: one per CTA whose unit range touches it
+    const int pair = qt >> 1;
+    const int nslots = first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles + a.f.rtiles - 1, a.f.U,
+                                    a.f.G) -
+                       first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles, a.f.U, a.f.G) + 1;
     int cnt = 0, nlog = 0;
-    if (lane < parts) {
+    if (lane < nslots) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
         nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
@@ -1682,10 +1695,9 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     const unsigned* gmax = refs.gmax;
 
     // 1. per-search state and the query-side prep
-    KNN_CUDA_CHECK(cudaMemsetAsync(part_cnt, 0, sizeof(int) * parts * TILE, stream));
-    KNN_CUDA_CHECK(cudaMemsetAsync(log_n, 0, sizeof(int) * parts * TILE, stream));
-    KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
-    KNN_CUDA_CHECK(cudaMemsetAsync(tglob, 0xff, sizeof(unsigned) * n_pad, stream));
+    // (no memsets: the query conversion initialises the cross-CTA bounds and
+    // the fallback counter; consumers read only the part slots a pair's CTAs
+    // actually wrote)
     PrepArgs pr{};
     pr.d = d;
     pr.Kp = L.Kp;
@@ -1698,6 +1710,8 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     pr.rows_pad = n_pad;
     pr.Xh = Qh;
     pr.qconst = qconst;
+    pr.tinit = tglob;
+    pr.zero = fb;
     {
         ProfileScope ps(stream, "prep_convert_queries");
         convert_kernel<true><<<static_cast<unsigned>(std::min<int64_t>((n_pad + 7) / 8, 8 * kSmCount)),
