@@ -312,7 +312,7 @@ struct FilterArgs {
     int2* log_h;           // [parts][128][CG] {group minimum bits, first reference index}
     int CG;                // log capacity (groups) per (part, query)
     int drain_at;          // drain when a lane holds this many group minima (<= CAP - 16)
-    int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work
+    int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work, 3 no pushes
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
     // large-k (filter_fixed_kernel): seed tiles per segment, per-query
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             w_[7]);                                                              \
             any_ |= gm_[i_] <= Tf;                                                               \
         }                                                                                        \
-        if (__any_sync(0xffffffffu, any_)) { /* some lane pushes: ~half the chunks */           \
+        if (a.mode != 3 && __any_sync(0xffffffffu, any_)) { /* some lane pushes: most chunks */ \
             _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                   \
                 push_group(gm_[i_], Tf, sg0 + static_cast<uint32_t>(nb) * (EPI_THREADS * 4),     \
                            ln < a.CG ? 1 : 0, lvp, lhp, vv + 8 * i_, (colb) + 8 * i_);           \
