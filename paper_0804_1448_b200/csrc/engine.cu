@@ -61,19 +61,12 @@ SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path)
     if (path != 1 && metric == kL2 && tensor_path_supported(n, m, d, k)) p.path = 2;
     if (path == 2 && p.path != 2 && metric == kL2 && !tensor_path_supported(n, m, d, k))
         p.path = 1;  // TENSOR requested for an unsupported shape: exact gives identical results
-    // exact path: split the reference axis until there are >= ~4 waves of
-    // CTAs (3 resident per SM); every split keeps >= max(k, 1024) references
-    const int64_t ctas_x = (n + exact_queries_per_cta() - 1) / exact_queries_per_cta();
-    const int64_t want = (4LL * kSmCount * 3 + ctas_x - 1) / ctas_x;
-    const int64_t max_splits = std::max<int64_t>(1, m / std::max<int64_t>(k, 1024));
-    p.splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, max_splits)));
-    p.splits = std::min(p.splits, 64);
     return p;
 }
 
 static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
-                      const float* dR, int64_t m, int d, int k, int metric, int splits,
-                      int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx) {
+                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                      int64_t index_base, float* d_out, int64_t* d_idx) {
     const bool big_k = static_cast<size_t>(k) > exact_smem_list_limit_k();
     ExactArgs a{};
     a.Q = dQ;
@@ -82,21 +75,21 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
     a.m = m;
     a.d = d;
     a.k = k;
-    a.splits = splits;
-    a.split_len = (m + splits - 1) / splits;
     a.index_base = index_base;
+    exact_plan(a, !big_k);
+    const int parts = a.parts;
 
     Sizer sz;
-    if (splits > 1) {
-        sz.take<float>(static_cast<size_t>(splits) * n * k);
-        sz.take<int64_t>(static_cast<size_t>(splits) * n * k);
+    if (parts > 1) {
+        sz.take<float>(static_cast<size_t>(parts) * n * k);
+        sz.take<int64_t>(static_cast<size_t>(parts) * n * k);
     }
-    const size_t lists = exact_cta_count(n, splits) * exact_queries_per_cta() * k;
+    const size_t lists = static_cast<size_t>(a.ctas) * exact_queries_per_cta() * k;
     if (big_k) {
         sz.take<float>(lists);
         sz.take<int32_t>(lists);
     }
-    if (splits > 1 && static_cast<size_t>(k) > 1024) {
+    if (parts > 1 && static_cast<size_t>(k) > 1024) {
         sz.take<float>(static_cast<size_t>(n) * k);
         sz.take<int64_t>(static_cast<size_t>(n) * k);
     }
@@ -104,9 +97,9 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
     Carver cv{static_cast<char*>(ctx.arena.base())};
     float* part_key = d_out;
     int64_t* part_idx = d_idx;
-    if (splits > 1) {
-        part_key = cv.take<float>(static_cast<size_t>(splits) * n * k);
-        part_idx = cv.take<int64_t>(static_cast<size_t>(splits) * n * k);
+    if (parts > 1) {
+        part_key = cv.take<float>(static_cast<size_t>(parts) * n * k);
+        part_idx = cv.take<int64_t>(static_cast<size_t>(parts) * n * k);
     }
     if (big_k) {
         a.glist_key = cv.take<float>(lists);
@@ -114,14 +107,14 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
     }
     a.out_key = part_key;
     a.out_idx = part_idx;
-    a.finalize = (splits == 1 && !raw_keys) ? 1 : 0;
+    a.finalize = (parts == 1 && !raw_keys) ? 1 : 0;
     launch_exact(metric, a, stream);
 
-    if (splits > 1) {
+    if (parts > 1) {
         MergeArgs mg{};
         mg.part_key = part_key;
         mg.part_idx = part_idx;
-        mg.parts = splits;
+        mg.parts = parts;
         mg.n = n;
         mg.k = k;
         mg.metric = metric;
@@ -148,17 +141,14 @@ void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int
             run_tensor_path(ctx, stream, dQ, n, dR, m, d, k, raw_keys, index_base, d_out, d_idx);
         return;
     }
-    run_exact(ctx, stream, dQ, n, dR, m, d, k, metric, plan.splits, raw_keys, index_base, d_out,
-              d_idx);
+    run_exact(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);
 }
 
 // exposed for the tensor path's fallback on uncertified queries
 void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                       const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
                       float* d_out, int64_t* d_idx) {
-    const SearchPlan plan = plan_search(n, m, d, k, kL2, 1);
-    run_exact(ctx, stream, dQ, n, dR, m, d, k, kL2, plan.splits, raw_keys, index_base, d_out,
-              d_idx);
+    run_exact(ctx, stream, dQ, n, dR, m, d, k, kL2, raw_keys, index_base, d_out, d_idx);
 }
 
 }  // namespace knnb200

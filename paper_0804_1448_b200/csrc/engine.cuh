@@ -60,7 +60,6 @@ DeviceContext& context_for(int device);  // device < 0: current device
 
 struct SearchPlan {
     int path;       // 1 exact, 2 tensor
-    int splits;     // reference-axis splits for the exact path
 };
 
 struct TensorRefs;

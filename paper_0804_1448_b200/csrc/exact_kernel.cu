@@ -5,15 +5,19 @@
 //                (src/bruteforce.cpp:23-38, include/knn/metric.hpp:22-44)
 //   HOT LOOP #2  select_k_smallest (src/topk.cpp:17-33)
 // The reference materialises a chunk x m row of double keys and selects per
-// row.  Here a CTA owns 64 queries, streams 128-reference tiles through
-// shared memory, computes the 64x128 key tile in registers (4x8 per thread,
-// coordinates in the reference's fixed order), and feeds each query's 128
-// keys to a warp-cooperative sorted top-k list (warp_list.cuh).  The n x m
-// key matrix never reaches HBM.
+// row.  Here a CTA owns 128 queries, streams 128-reference tiles through a
+// cp.async shared-memory pipeline, computes the 128x128 key tile in registers
+// (8x8 per thread, packed FP32 pairs, coordinates in the reference's fixed
+// order), and offers each query's keys that beat its running threshold to a
+// warp-cooperative sorted top-k list (warp_list.cuh) straight from registers.
+// The n x m key matrix never reaches HBM.
 //
 // This is the engine's exact path: all metrics, any k, any d.  It is also the
 // certification fallback of the tensor path (tensor_kernel.cu) and the
 // re-rank arithmetic reference (key_step<M> in common.cuh).
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "exact_kernel.cuh"
 #include "profile.cuh"
@@ -23,164 +27,331 @@ namespace knnb200 {
 
 namespace {
 
-constexpr int QT = 64;    // queries per CTA
+// CTA tile: 128 queries x 128 references, 256 threads, 8 x 8 keys per thread
+// (rows ty + 16 i, reference pairs tx + 16 jp).  Coordinates stream through a
+// two-stage cp.async pipeline in 32-coordinate chunks:
+//   Q stage  [128 rows][QP]        row-major (reads are 2-address broadcasts)
+//   R stage  [64 pairs][RPS]       two references interleaved per coordinate:
+//                                  r0c0 r1c0 r0c1 r1c1 ...  so one 16-byte
+//                                  load yields the packed pairs (r0,r1) at c
+//                                  and c+1 -- the operand shape of the sm_100
+//                                  packed FADD2/FFMA2 (fma.rn.f32x2) with the
+//                                  query coordinate as the broadcast scalar.
+// Every key is still accumulated coordinate by coordinate in ascending order
+// with round-to-nearest sub + fma (key_step<M>), so keys are bit-identical to
+// the scalar formulation used by the re-rank and merge paths.
+constexpr int QT = 128;   // queries per CTA
 constexpr int RT = 128;   // references per tile
-constexpr int DC = 8;     // coordinates per staged chunk
-constexpr int QS = QT + 4;
-constexpr int RS = RT + 4;
-constexpr int DS = RT + 4;  // distance-tile row stride (bank-conflict free)
+constexpr int DC = 32;    // coordinates per stage
+constexpr int QP = DC + 4;                 // Q row pitch (floats): 144 B, rows ty / ty+1 in distinct banks
+constexpr int RPS = 2 * DC + 4;            // R pair pitch (floats): 272 B, 8 pairs -> 8 distinct 16 B bank groups
+constexpr int QSTAGE = QT * QP;
+constexpr int RSTAGE = (RT / 2) * RPS;
+constexpr int STAGE = QSTAGE + RSTAGE;     // floats per pipeline stage
+constexpr int NSTAGE = 2;
 constexpr int THREADS = 256;
+constexpr int LOADS = QT * DC / THREADS;   // 4-byte cp.async per operand per thread per stage
 
-template <int M, bool SMEM_LISTS>
-__global__ void __launch_bounds__(THREADS) exact_knn_kernel(ExactArgs a) {
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Two key_step<M> updates at once: acc.{x,y} = key_step(acc.{x,y}, q, r.{x,y}).
+// For L2 this is one packed FADD2 (q broadcast, r negated by an operand
+// modifier: q + (-r) == q - r exactly) and one packed FFMA2.
+template <int M>
+__device__ __forceinline__ float2 key_step2(float2 acc, float q, float2 r) {
+    if constexpr (M == kL2) {
+        const float2 t = __fadd2_rn(make_float2(q, q), make_float2(-r.x, -r.y));
+        return __ffma2_rn(t, t, acc);
+    } else {
+        return make_float2(key_step<M>(acc.x, q, r.x), key_step<M>(acc.y, q, r.y));
+    }
+}
+
+// KP: list entries per lane of the register-resident list (k <= 32 KP, lists in
+// shared memory), or 0 for lists in global memory (k > 128, WarpList).
+template <int M, int KP>
+__global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
+    constexpr bool SMEM_LISTS = KP > 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* Qs = reinterpret_cast<float*>(smem_raw);          // [DC][QS]
-    float* Rs = Qs + DC * QS;                                  // [DC][RS]
-    float* Ds = Rs + DC * RS;                                  // [QT][DS]
-    float* Lk = Ds + QT * DS;                                  // [QT][k] (smem lists)
+    float* stages = reinterpret_cast<float*>(smem_raw);      // [NSTAGE][STAGE]
+    float* Lk = stages + NSTAGE * STAGE;                       // [QT][k] (smem lists)
     int32_t* Li = reinterpret_cast<int32_t*>(Lk + (SMEM_LISTS ? QT * a.k : 0));
+    float* sc = reinterpret_cast<float*>(Li + (SMEM_LISTS ? QT * a.k : 0)) + (threadIdx.x >> 5) * 2 * RT;
+    const uint32_t stage_base = static_cast<uint32_t>(__cvta_generic_to_shared(stages));
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int ty = tid >> 4;
-    const int tx = tid & 15;
+    const int ty = tid >> 4;   // rows ty + 16 i      (warp w: ty = 2w, 2w + 1)
+    const int tx = tid & 15;   // pairs tx + 16 jp    (references 2 (tx + 16 jp) + e)
+    const int half = lane >> 4;
 
-    const int64_t q0 = static_cast<int64_t>(blockIdx.x) * QT;
-    const int split = blockIdx.y;
-    const int64_t r_lo = static_cast<int64_t>(split) * a.split_len;
-    const int64_t r_hi = min(a.m, r_lo + a.split_len);
     const int d = a.d;
-
+    const int64_t m = a.m;
     if constexpr (!SMEM_LISTS) {
-        const size_t cta = static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x;
-        Lk = a.glist_key + cta * QT * a.k;
-        Li = a.glist_idx + cta * QT * a.k;
+        Lk = a.glist_key + static_cast<size_t>(blockIdx.x) * QT * a.k;
+        Li = a.glist_idx + static_cast<size_t>(blockIdx.x) * QT * a.k;
     }
+    const int nchunks = (d + DC - 1) / DC;
+    const int rr = 2 * (tid >> 6) + (tid & 1);
+    const int rc = (tid & 63) >> 1;
 
-    // this warp's 8 query lists
-    for (int rr = 0; rr < 8; ++rr) {
-        const int row = warp * 8 + rr;
-        WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
-        L.init(lane);
-    }
+    // stream-K: this CTA owns units [u, u_end) of the (query block, tile)
+    // sequence; each query block it touches is one segment with its own lists
+    const int64_t W = a.units;
+    const int64_t G = gridDim.x;
+    int64_t u = static_cast<int64_t>(blockIdx.x) * W / G;
+    const int64_t u_end = static_cast<int64_t>(blockIdx.x + 1) * W / G;
+    auto cta_of = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
 
-    for (int64_t t0 = r_lo; t0 < r_hi; t0 += RT) {
-        float acc[4][8];
-#pragma unroll
-        for (int qi = 0; qi < 4; ++qi)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[qi][j] = 0.f;
+    int buf = 0;
+    while (u < u_end) {
+        const int64_t b = u / a.ntiles;
+        const int t_a = static_cast<int>(u - b * a.ntiles);
+        const int t_b = static_cast<int>(min(static_cast<int64_t>(a.ntiles), t_a + (u_end - u)));
+        u += t_b - t_a;
+        const int64_t q0 = b * QT;
+        const int64_t first = cta_of(b * a.ntiles);
+        const int part = static_cast<int>(blockIdx.x - first);
+        const int nparts = static_cast<int>(cta_of((b + 1) * a.ntiles - 1) - first + 1);
 
-        for (int c0 = 0; c0 < d; c0 += DC) {
-            // stage Q chunk (64 x 8) and R chunk (128 x 8), transposed, zero-filled
-#pragma unroll
-            for (int s = 0; s < (QT * DC) / THREADS; ++s) {
-                const int e = tid + s * THREADS;
-                const int row = e / DC, c = e % DC;
-                const int64_t gq = q0 + row;
-                const int gc = c0 + c;
-                Qs[c * QS + row] = (gq < a.n && gc < d) ? __ldg(a.Q + gq * d + gc) : 0.f;
+        // warp w owns rows 2w + h + 16 i (h < 2, i < 8): its 16 lists are private
+        for (int i = 0; i < 8; ++i)
+            for (int h = 0; h < 2; ++h) {
+                const int row = 2 * warp + h + 16 * i;
+                WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
+                L.init(lane);
             }
-#pragma unroll
-            for (int s = 0; s < (RT * DC) / THREADS; ++s) {
-                const int e = tid + s * THREADS;
-                const int row = e / DC, c = e % DC;
-                const int64_t gr = t0 + row;
-                const int gc = c0 + c;
-                Rs[c * RS + row] = (gr < r_hi && gc < d) ? __ldg(a.R + gr * d + gc) : 0.f;
+        __syncwarp();
+
+        // stage loader: Q rows q0.. (row-major, 32 coords) and R rows t0..
+        // (pair-interleaved).  Load s of this thread covers Q row 8 s + warp,
+        // coordinate lane, and R reference t0 + 8 s + rr, coordinate rc, where a
+        // warp reads 128 contiguous bytes of Q and 2 x 64 bytes of R.
+        const int nq = static_cast<int>(min(static_cast<int64_t>(QT), a.n - q0));
+        auto issue = [&](int tile, int chunk, int sb) {
+            const int64_t t0 = static_cast<int64_t>(tile) * RT;
+            const int nr = static_cast<int>(min(static_cast<int64_t>(RT), m - t0));
+            const int c0 = chunk * DC;
+            const uint32_t sq = stage_base + static_cast<uint32_t>(sb * STAGE) * 4u;
+            const uint32_t sr = sq + QSTAGE * 4u;
+            const bool okq_c = c0 + lane < d, okr_c = c0 + rc < d;
+            const float* gq = a.Q + (q0 + warp) * d + c0 + lane;
+            const float* gr = a.R + (t0 + rr) * d + c0 + rc;
+            uint32_t dq = sq + static_cast<uint32_t>(warp * QP + lane) * 4u;
+            uint32_t dr = sr + static_cast<uint32_t>((tid >> 6) * RPS + (tid & 63)) * 4u;
+#pragma unroll 1
+            for (int s = 0; s < LOADS; ++s) {
+                const bool okq = okq_c && 8 * s + warp < nq;
+                const bool okr = okr_c && 8 * s + rr < nr;
+                cp_async4(dq, okq ? gq : a.Q, okq);
+                cp_async4(dr, okr ? gr : a.R, okr);
+                gq += 8 * static_cast<int64_t>(d);
+                gr += 8 * static_cast<int64_t>(d);
+                dq += 8 * QP * 4;
+                dr += 4 * RPS * 4;
             }
-            __syncthreads();
+            cp_async_commit();
+        };
+
+        float2 acc[8][4];
 #pragma unroll
-            for (int c = 0; c < DC; ++c) {
-                const float4 qv = *reinterpret_cast<const float4*>(Qs + c * QS + ty * 4);
-                float rv[8];
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) rv[j] = Rs[c * RS + tx + 16 * j];
-                const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+            for (int jp = 0; jp < 4; ++jp) acc[i][jp] = make_float2(0.f, 0.f);
+
+        // the buffer `buf` was last read two chunks ago, behind a barrier
+        issue(t_a, 0, buf);
+        for (int tile = t_a; tile < t_b; ++tile)
+        for (int chunk = 0; chunk < nchunks; ++chunk, buf ^= 1) {
+            cp_async_wait_all();
+            __syncthreads();  // this stage landed for all threads; the previous one fully consumed
+            if (chunk + 1 < nchunks) issue(tile, chunk + 1, buf ^ 1);
+            else if (tile + 1 < t_b) issue(tile + 1, 0, buf ^ 1);
+
+            const int c0 = chunk * DC;
+            const int ng = (min(DC, d - c0) + 1) >> 1;  // coordinate pairs (a zero-filled odd tail is a no-op)
+            const float* Qs = stages + buf * STAGE;
+            const float* Rs = Qs + QSTAGE;
+#pragma unroll 1
+            for (int g = 0; g < ng; ++g) {
+                float2 qv[8];
 #pragma unroll
-                for (int qi = 0; qi < 4; ++qi)
+                for (int i = 0; i < 8; ++i)
+                    qv[i] = *reinterpret_cast<const float2*>(Qs + (ty + 16 * i) * QP + 2 * g);
+                float2 r01[4], r23[4];  // (ref pair) at coordinates 2g and 2g + 1
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[qi][j] = key_step<M>(acc[qi][j], qq[qi], rv[j]);
+                for (int jp = 0; jp < 4; ++jp) {
+                    const float4 v = *reinterpret_cast<const float4*>(Rs + (tx + 16 * jp) * RPS + 4 * g);
+                    r01[jp] = make_float2(v.x, v.y);
+                    r23[jp] = make_float2(v.z, v.w);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp) {
+                        acc[i][jp] = key_step2<M>(acc[i][jp], qv[i].x, r01[jp]);
+                        acc[i][jp] = key_step2<M>(acc[i][jp], qv[i].y, r23[jp]);
+                    }
             }
-            __syncthreads();
+
+            if (chunk == nchunks - 1) {
+                // tile complete: fused selection straight from registers.  Lane
+                // (tx, half) holds 8 keys of row 2 warp + half + 16 i; the warp
+                // votes against the rows' running thresholds (the lists' k-th
+                // keys) and only offers a row pair's keys when one can enter.
+                const int64_t t0 = static_cast<int64_t>(tile) * RT;
+                const int64_t rem = m - t0;
+                if (rem < RT) {  // partial last tile: columns past r_hi hold zero-filled keys
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp) {
+                        const int col = 2 * (tx + 16 * jp);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            if (col >= rem) acc[i][jp].x = kInf;
+                            if (col + 1 >= rem) acc[i][jp].y = kInf;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float mn = fminf(acc[i][0].x, acc[i][0].y);
+#pragma unroll
+                    for (int jp = 1; jp < 4; ++jp) mn = fminf(mn, fminf(acc[i][jp].x, acc[i][jp].y));
+                    const float thr = Lk[(2 * warp + half + 16 * i) * a.k + a.k - 1];
+                    const unsigned vote = __ballot_sync(0xffffffffu, mn <= thr);
+                    if (vote == 0u) continue;
+                    // stage the row pair's 2 x 128 keys in the warp's scratch
+                    // and offer each row 4 keys per lane (the list is loaded
+                    // into registers for the burst: WarpRegList)
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp)
+                        *reinterpret_cast<float2*>(sc + half * RT + 2 * (tx + 16 * jp)) = acc[i][jp];
+                    __syncwarp();
+                    for (int h = 0; h < 2; ++h) {
+                        if (((vote >> (16 * h)) & 0xffffu) == 0u) continue;
+                        const int row = 2 * warp + h + 16 * i;
+                        if constexpr (KP > 0) {
+                            float ck[4];
+                            int32_t ci[4];
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const int col = lane + 32 * p;
+                                const bool ok = col < rem;
+                                ck[p] = ok ? sc[h * RT + col] : kInf;
+                                ci[p] = ok ? static_cast<int32_t>(t0 + col) : 0x7fffffff;
+                            }
+                            WarpRegList<KP> L;
+                            L.load(Lk + row * a.k, Li + row * a.k, a.k, lane);
+                            if (L.offer<4>(ck, ci, a.k, lane)) L.store(Lk + row * a.k, Li + row * a.k, a.k, lane);
+                        } else {
+                            float ck[4];
+                            int64_t ci[4];
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const int col = lane + 32 * p;
+                                const bool ok = col < rem;
+                                ck[p] = ok ? sc[h * RT + col] : kInf;
+                                ci[p] = ok ? t0 + col : kSentinelIdx;
+                            }
+                            WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
+                            L.offer<4>(ck, ci, lane);
+                        }
+                    }
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp) acc[i][jp] = make_float2(0.f, 0.f);
+            }
         }
+        __syncwarp();
 
-#pragma unroll
-        for (int qi = 0; qi < 4; ++qi)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) Ds[(ty * 4 + qi) * DS + tx + 16 * j] = acc[qi][j];
-        __syncthreads();
-
-        // fused selection: warp w owns rows 8w .. 8w+7
-        for (int rr = 0; rr < 8; ++rr) {
-            const int row = warp * 8 + rr;
-            if (q0 + row >= a.n) break;
-            float ck[4];
-            int64_t ci[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const int col = lane + 32 * p;
-                const int64_t j = t0 + col;
-                const bool ok = j < r_hi;
-                ck[p] = ok ? Ds[row * DS + col] : kInf;
-                ci[p] = ok ? j : kSentinelIdx;
+        // emit this warp's lists into output slot `part` (raw keys for the
+        // merge, or finalized when every query block is one segment); the
+        // block's first CTA pads the slots its block does not use
+        for (int i = 0; i < 8; ++i)
+            for (int h = 0; h < 2; ++h) {
+                const int row = 2 * warp + h + 16 * i;
+                const int64_t q = q0 + row;
+                if (q >= a.n) continue;
+                const size_t base = (static_cast<size_t>(part) * a.n + q) * a.k;
+                if (a.finalize) finalize_list(Lk + row * a.k, Li + row * a.k, a.k, M, lane);
+                for (int t = lane; t < a.k; t += 32) {
+                    const float key = Lk[row * a.k + t];
+                    const int32_t li = Li[row * a.k + t];
+                    a.out_key[base + t] = key;
+                    a.out_idx[base + t] = li == 0x7fffffff ? kSentinelIdx : a.index_base + li;
+                }
+                if (part == 0)
+                    for (int pp = nparts; pp < a.parts; ++pp) {
+                        const size_t pb = (static_cast<size_t>(pp) * a.n + q) * a.k;
+                        for (int t = lane; t < a.k; t += 32) {
+                            a.out_key[pb + t] = kInf;
+                            a.out_idx[pb + t] = kSentinelIdx;
+                        }
+                    }
             }
-            WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
-            L.offer<4>(ck, ci, lane);
-        }
-        // no barrier needed: the next tile's Ds write is behind the c-loop barriers
+        __syncwarp();
     }
-    __syncwarp();
+}
 
-    // emit this warp's lists: raw keys for a later merge, or finalized
-    for (int rr = 0; rr < 8; ++rr) {
-        const int row = warp * 8 + rr;
-        const int64_t q = q0 + row;
-        if (q >= a.n) break;
-        const size_t base = (static_cast<size_t>(split) * a.n + q) * a.k;
-        if (a.finalize) finalize_list(Lk + row * a.k, Li + row * a.k, a.k, M, lane);
-        for (int t = lane; t < a.k; t += 32) {
-            const float key = Lk[row * a.k + t];
-            const int32_t li = Li[row * a.k + t];
-            a.out_key[base + t] = key;
-            a.out_idx[base + t] = li == 0x7fffffff ? kSentinelIdx : a.index_base + li;
-        }
-    }
+size_t smem_bytes(int k, bool smem_lists) {
+    const size_t stages = static_cast<size_t>(NSTAGE) * STAGE * sizeof(float);
+    const size_t lists = static_cast<size_t>(QT) * k * (sizeof(float) + sizeof(int32_t));
+    const size_t scratch = static_cast<size_t>(THREADS / 32) * 2 * RT * sizeof(float);
+    return stages + (smem_lists ? lists : 0) + scratch;
 }
 
 template <int M>
 void launch_exact_m(const ExactArgs& a, cudaStream_t stream) {
-    const size_t tiles = static_cast<size_t>(DC) * (QS + RS) + static_cast<size_t>(QT) * DS;
-    const size_t list_bytes = static_cast<size_t>(QT) * a.k * (sizeof(float) + sizeof(int32_t));
     const bool smem_lists = a.glist_key == nullptr;
-    const size_t smem = tiles * sizeof(float) + (smem_lists ? list_bytes : 0);
-    dim3 grid(static_cast<unsigned>((a.n + QT - 1) / QT), static_cast<unsigned>(a.splits));
-    if (smem_lists) {
-        auto kern = exact_knn_kernel<M, true>;
-        KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        ProfileScope ps(stream, "exact_knn_kernel");
-        kern<<<grid, THREADS, smem, stream>>>(a);
-    } else {
-        auto kern = exact_knn_kernel<M, false>;
-        KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        ProfileScope ps(stream, "exact_knn_kernel_glist");
-        kern<<<grid, THREADS, smem, stream>>>(a);
-    }
+    const size_t smem = smem_bytes(a.k, smem_lists);
+    const dim3 grid(static_cast<unsigned>(a.ctas));
+    const int kp = (a.k + 31) / 32;
+    void (*kern)(ExactArgs) = !smem_lists ? exact_knn_kernel<M, 0>
+                              : kp == 1   ? exact_knn_kernel<M, 1>
+                              : kp == 2   ? exact_knn_kernel<M, 2>
+                                          : exact_knn_kernel<M, 4>;
+    KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    ProfileScope ps(stream, smem_lists ? "exact_knn_kernel" : "exact_knn_kernel_glist");
+    kern<<<grid, THREADS, smem, stream>>>(a);
     KNN_LAUNCH_CHECK();
 }
 
 }  // namespace
 
 size_t exact_smem_list_limit_k() {
-    // keep lists in shared memory while 64 queries x k x 8 B <= 64 KB
+    // lists in shared memory while 128 queries x k x 8 B + the stages fit 227 KB
     return 128;
 }
 
-size_t exact_cta_count(int64_t n, int splits) {
-    return static_cast<size_t>((n + QT - 1) / QT) * static_cast<size_t>(splits);
+void exact_plan(ExactArgs& a, bool smem_lists) {
+    // resident CTAs: 2 per SM while the shared-memory footprint allows it
+    const size_t smem = smem_bytes(a.k, smem_lists);
+    const int per_sm = smem <= 113 * 1024 ? 2 : 1;  // 228 KB per SM, 1 KB reserved per CTA
+    const int64_t nqb = (a.n + QT - 1) / QT;
+    a.ntiles = static_cast<int>((a.m + RT - 1) / RT);
+    a.units = nqb * a.ntiles;
+    // every CTA keeps >= 8 tiles (1024 references) so lists amortise their fill
+    const int64_t by_work = std::max<int64_t>(1, a.units / 8);
+    a.ctas = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(kSmCount) * per_sm, by_work));
+    // parts: the most CTAs any query block is spread over
+    const int64_t W = a.units, G = a.ctas;
+    auto cta_of = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
+    int parts = 1;
+    for (int64_t b = 0; b < nqb; ++b)
+        parts = std::max<int>(parts, static_cast<int>(cta_of((b + 1) * a.ntiles - 1) -
+                                                      cta_of(b * a.ntiles) + 1));
+    a.parts = parts;
 }
 
 int exact_queries_per_cta() { return QT; }

@@ -11,19 +11,22 @@ struct ExactArgs {
     const float* R;          // m x d
     int64_t n, m;
     int d, k;
-    int64_t split_len;       // references per blockIdx.y split (>= k)
-    int splits;
+    int64_t units;           // stream-K work units: query blocks x reference tiles
+    int ntiles;              // reference tiles per query block
+    int ctas;                // grid size (each CTA owns a contiguous unit range)
+    int parts;               // output slots per query (max CTAs sharing a query block)
     int64_t index_base;      // added to every emitted index
-    float* out_key;          // [splits][n][k]
-    int64_t* out_idx;        // [splits][n][k]
-    int finalize;            // 1: out_key = finalized distance (splits == 1 only)
+    float* out_key;          // [parts][n][k]
+    int64_t* out_idx;        // [parts][n][k]
+    int finalize;            // 1: out_key = finalized distance (parts == 1 only)
     float* glist_key;        // global list scratch when k is too large for smem
     int32_t* glist_idx;
 };
 
+// Work split of the exact kernel over the GPU: fills units/ntiles/ctas/parts.
+void exact_plan(ExactArgs& a, bool smem_lists);
 void launch_exact(int metric, const ExactArgs& a, cudaStream_t stream);
 size_t exact_smem_list_limit_k();
-size_t exact_cta_count(int64_t n, int splits);
 int exact_queries_per_cta();
 
 struct MergeArgs {

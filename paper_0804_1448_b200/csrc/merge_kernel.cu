@@ -1,9 +1,9 @@
 // merge_kernel.cu -- merge per-part top-k lists into the final top-k.
 //
-// Used for (a) the reference-axis splits of one GPU's search (wave
-// balancing) and (b) the shard merge of a reference-sharded multi-GPU search
-// after the all-gather.  Each part's list is the top-k of a
-// disjoint reference range, sorted under the (key, index) order
+// Used for (a) the stream-K parts of one GPU's exact search (a query block
+// spread over several CTAs) and (b) the shard merge of a reference-sharded
+// multi-GPU search after the all-gather.  Each part's list
+// is the top-k of a disjoint reference range, sorted under the (key, index) order
 // (topk.cpp:11-13); the top-k of the union equals the top-k of the union of
 // the part top-ks, so the result is bitwise independent of how the
 // reference set was split.

@@ -121,6 +121,130 @@ struct WarpList {
     }
 };
 
+// Register-resident variant for a burst of offers to one list with k <= 32 P:
+// the list (same storage and order as WarpList) is loaded into registers,
+// entry e = lane + 32 j in key[j] / idx[j], updated with warp shuffles (no
+// shared-memory round trip per insertion) and written back once.
+template <int P>
+struct WarpRegList {
+    float key[P];
+    int32_t idx[P];
+
+    __device__ __forceinline__ void load(const float* lk, const int32_t* li, int k, int lane) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const int e = lane + 32 * j;
+            key[j] = e < k ? lk[e] : kInf;
+            idx[j] = e < k ? li[e] : 0x7fffffff;
+        }
+    }
+    __device__ __forceinline__ void store(float* lk, int32_t* li, int k, int lane) const {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const int e = lane + 32 * j;
+            if (e < k) {
+                lk[e] = key[j];
+                li[e] = idx[j];
+            }
+        }
+    }
+    // k-th entry (the running threshold), on every lane
+    __device__ __forceinline__ void threshold(int k, float& tk, int32_t& ti) const {
+        const int e = k - 1, j = e >> 5;
+        float kk = key[0];
+        int32_t ii = idx[0];
+#pragma unroll
+        for (int jj = 1; jj < P; ++jj)
+            if (jj == j) {
+                kk = key[jj];
+                ii = idx[jj];
+            }
+        tk = __shfl_sync(0xffffffffu, kk, e & 31);
+        ti = __shfl_sync(0xffffffffu, ii, e & 31);
+    }
+    // insert (x, jx) (same on all lanes), known to beat the threshold
+    __device__ __forceinline__ void insert(float x, int32_t jx, int k, int lane) {
+        int pos = 0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const bool lt = lane + 32 * j < k && pair_less(key[j], idx[j], x, jx);
+            pos += __popc(__ballot_sync(0xffffffffu, lt));
+        }
+        float pk[P];
+        int32_t pi[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) {  // predecessor of entry e (entry e - 1), from the old values
+            pk[j] = __shfl_up_sync(0xffffffffu, key[j], 1);
+            pi[j] = __shfl_up_sync(0xffffffffu, idx[j], 1);
+            if (j > 0) {
+                const float ck = __shfl_sync(0xffffffffu, key[j - 1], 31);
+                const int32_t cj = __shfl_sync(0xffffffffu, idx[j - 1], 31);
+                if (lane == 0) {
+                    pk[j] = ck;
+                    pi[j] = cj;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const int e = lane + 32 * j;
+            if (e > pos) {
+                key[j] = pk[j];
+                idx[j] = pi[j];
+            } else if (e == pos) {
+                key[j] = x;
+                idx[j] = jx;
+            }
+        }
+    }
+    // Offer up to 32 x C candidates held C per lane (invalid = +inf / INT32_MAX);
+    // inserts every one that beats the running threshold.  Returns whether the
+    // list changed.
+    template <int C>
+    __device__ bool offer(const float (&ck)[C], const int32_t (&ci)[C], int k, int lane) {
+        float tk;
+        int32_t ti;
+        threshold(k, tk, ti);
+        unsigned pending = 0;
+#pragma unroll
+        for (int p = 0; p < C; ++p)
+            if (pair_less(ck[p], ci[p], tk, ti)) pending |= 1u << p;
+        bool changed = false;
+        while (__any_sync(0xffffffffu, pending != 0)) {
+            float myk = kInf;
+            int32_t myi = 0x7fffffff;
+            int myp = -1;
+            if (pending) {
+                myp = __ffs(pending) - 1;
+#pragma unroll
+                for (int p = 0; p < C; ++p)
+                    if (p == myp) {
+                        myk = ck[p];
+                        myi = ci[p];
+                    }
+            }
+            unsigned who = __ballot_sync(0xffffffffu, pending != 0);
+            while (who) {
+                const int src = __ffs(who) - 1;
+                who &= who - 1;
+                const float x = __shfl_sync(0xffffffffu, myk, src);
+                const int32_t jx = __shfl_sync(0xffffffffu, myi, src);
+                if (pair_less(x, jx, tk, ti)) {
+                    insert(x, jx, k, lane);
+                    threshold(k, tk, ti);
+                    changed = true;
+                }
+            }
+            if (myp >= 0) pending &= ~(1u << myp);
+#pragma unroll
+            for (int p = 0; p < C; ++p)
+                if ((pending >> p) & 1u)
+                    if (!pair_less(ck[p], ci[p], tk, ti)) pending &= ~(1u << p);
+        }
+        return changed;
+    }
+};
+
 // Finalize a sorted list in place (sqrt for L2) and restore the reference's
 // table invariant (test_bruteforce.cpp:22-39: equal reported distances appear
 // in ascending index order).  Two distinct squared keys can round to the same
