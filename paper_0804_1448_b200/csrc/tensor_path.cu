@@ -1018,7 +1018,107 @@ constexpr int LK_THREADS = 512;
 #define KNN_DBG_LARGE 0
 #endif
 
-__device__ void bitonic_sort_kv(float* key, int* idx, int N) {  // N power of two, block-wide
+// Bitonic sort of N (power of two) (key, index) pairs in shared memory under
+// the (key, index) order, by `nthreads` threads (32: one warp, no block
+// barriers; or the whole block).  Thread t holds elements t E .. t E + E - 1 in
+// registers (E = N / nthreads): strides below E are register swaps, strides
+// below 32 E are lane shuffles, and only the strides that cross warps go
+// through shared memory (one barrier each) -- 18 barriers at N = 2048 where the
+// all-shared-memory network needs 66.
+template <int E>
+__device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) {
+    const int t = threadIdx.x;
+    const bool active = t < nthreads;
+    const int W = 32 * E;  // elements per warp
+    float rk[E];
+    int ri[E];
+    __syncthreads();  // the caller's writes of key/idx are visible
+    if (active)
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            rk[j] = key[t * E + j];
+            ri[j] = idx[t * E + j];
+        }
+    for (int size = 2; size <= N; size <<= 1) {
+        int stride = size >> 1;
+        if (stride >= W) {  // cross-warp strides (nthreads > 32 only)
+            __syncthreads();  // everyone is done reading the previous shared phase
+            if (active)
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    key[t * E + j] = rk[j];
+                    idx[t * E + j] = ri[j];
+                }
+            for (; stride >= W; stride >>= 1) {
+                __syncthreads();
+                for (int i = t; i < (N >> 1); i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1));
+                    const int hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const float ka = key[lo], kb = key[hi];
+                    const int ia = idx[lo], ib = idx[hi];
+                    if (pair_less(kb, ib, ka, ia) == up) {
+                        key[lo] = kb;
+                        key[hi] = ka;
+                        idx[lo] = ib;
+                        idx[hi] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+            if (active)
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    rk[j] = key[t * E + j];
+                    ri[j] = idx[t * E + j];
+                }
+        }
+        if (!active) continue;
+        for (; stride >= E; stride >>= 1) {  // partner in lane ^ (stride / E), same slot
+            const int lm = stride / E;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const float pk = __shfl_xor_sync(0xffffffffu, rk[j], lm);
+                const int pi = __shfl_xor_sync(0xffffffffu, ri[j], lm);
+                const int e = t * E + j;
+                const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+                const bool p_less = pair_less(pk, pi, rk[j], ri[j]);
+                if (p_less == keep_min) {
+                    rk[j] = pk;
+                    ri[j] = pi;
+                }
+            }
+        }
+#pragma unroll
+        for (int s = E / 2; s > 0; s >>= 1) {  // partner in this thread
+            if (s > stride) continue;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                if (j & s) continue;
+                const bool up = ((t * E + j) & size) == 0;
+                if (pair_less(rk[j + s], ri[j + s], rk[j], ri[j]) == up) {
+                    const float tk = rk[j];
+                    const int ti = ri[j];
+                    rk[j] = rk[j + s];
+                    ri[j] = ri[j + s];
+                    rk[j + s] = tk;
+                    ri[j + s] = ti;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (active)
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            key[t * E + j] = rk[j];
+            idx[t * E + j] = ri[j];
+        }
+    __syncthreads();
+}
+
+// All-shared-memory network (one barrier per stage), kept for comparison.
+__device__ void bitonic_sort_kv_smem(float* key, int* idx, int N) {
     for (int size = 2; size <= N; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             __syncthreads();
@@ -1028,8 +1128,7 @@ __device__ void bitonic_sort_kv(float* key, int* idx, int N) {  // N power of tw
                 const bool up = (lo & size) == 0;
                 const float ka = key[lo], kb = key[hi];
                 const int ia = idx[lo], ib = idx[hi];
-                const bool gt = pair_less(kb, ib, ka, ia);  // (a > b)
-                if (gt == up) {
+                if (pair_less(kb, ib, ka, ia) == up) {
                     key[lo] = kb;
                     key[hi] = ka;
                     idx[lo] = ib;
@@ -1039,6 +1138,26 @@ __device__ void bitonic_sort_kv(float* key, int* idx, int N) {  // N power of tw
         }
     }
     __syncthreads();
+}
+
+// N (power of two, 32 <= N <= 16 * blockDim.x) pairs by the whole block:
+// one element per thread up to N = blockDim.x, then N / blockDim.x.
+__device__ void bitonic_sort_kv(float* key, int* idx, int N, int variant) {
+    if (variant == 1) {
+        bitonic_sort_kv_smem(key, idx, N);
+        return;
+    }
+    const int bd = static_cast<int>(blockDim.x);
+    if (N <= bd) {
+        bitonic_sort_kv_regs<1>(key, idx, N, N);
+        return;
+    }
+    switch (N / bd) {
+        case 2: bitonic_sort_kv_regs<2>(key, idx, N, bd); break;
+        case 4: bitonic_sort_kv_regs<4>(key, idx, N, bd); break;
+        case 8: bitonic_sort_kv_regs<8>(key, idx, N, bd); break;
+        default: bitonic_sort_kv_regs<16>(key, idx, N, bd); break;
+    }
 }
 
 // k-th smallest (1-based) of x[0..n) (finite floats), block-wide radix select
@@ -1113,6 +1232,7 @@ struct LargeArgs {
     int* fb_count;
     int* fb_list;
     int fb_offset;
+    int sort_variant;        // dev: 1 = all-shared-memory bitonic network
 };
 
 __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
@@ -1212,13 +1332,13 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
         }
         sk[c] = acc;
     }
-    int N2 = 1;
+    int N2 = 32;
     while (N2 < nc) N2 <<= 1;
     for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
         sk[e] = kInf;
         si[e] = 0x7fffffff;
     }
-    bitonic_sort_kv(sk, si, N2);
+    bitonic_sort_kv(sk, si, N2, a.sort_variant);
     // finalize: sqrt, then equal reported distances in ascending index order
     if (!a.raw_keys) {
         for (int t = threadIdx.x; t < k; t += blockDim.x) sk[t] = __fsqrt_rn(sk[t]);
@@ -1797,6 +1917,11 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         la.d = d;
         la.k = k;
         la.S_max = S_max;
+        static const int sort_variant = [] {
+            const char* e = getenv("KNN_B200_SORT");
+            return e ? atoi(e) : 0;
+        }();
+        la.sort_variant = sort_variant;
         int NC = 1;
         while (NC < 2 * margin * k) NC <<= 1;
         NC = std::min(NC, 16 * LK_THREADS);
