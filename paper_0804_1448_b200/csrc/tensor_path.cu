@@ -947,52 +947,56 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t taddr = tlane + static_cast<uint32_t>(b * TILE);
             const int col_base = sq.tile() * TILE;
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                uint32_t r0[32], r1[32];
-                sm100::tmem_ld_32x32b_x32(taddr + h * 64, r0);
-                sm100::tmem_ld_32x32b_x32(taddr + h * 64 + 32, r1);
+            for (int h = 0; h < 4; ++h) {  // 32-column chunks (one TMEM load each)
+                uint32_t r0[32];
+                sm100::tmem_ld_32x32b_x32(taddr + h * 32, r0);
                 sm100::tmem_ld_wait();
-                if (h == 1) {
+                if (h == 3) {
                     sm100::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
                 }
-                float v[2][32];
+                float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v[0][j] = __uint_as_float(r0[j]);
-                    v[1][j] = __uint_as_float(r1[j]);
-                }
-                const int cb = col_base + h * 64;
-                if (!a.fold) {
-                    add_rnorm(v[0], a.rnorm + cb);
-                    add_rnorm(v[1], a.rnorm + cb + 32);
-                }
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
+                const int cb = col_base + h * 32;
+                if (!a.fold) add_rnorm(v, a.rnorm + cb);
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int g = 0; g < 4; ++g) {
+                    const float* w = v + 8 * g;
+                    const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
+                    if (seed) {
+                        S.insert(gm);
+                    } else if (__any_sync(0xffffffffu, gm <= T0)) {
+                        const int col = cb + 8 * g;
+                        if (ln + 8 <= a.CV) {  // room for the whole group: 3 instructions per value
+                            float2* const v0 = vlp;
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const float* w = v[c] + 8 * g;
-                        const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]),
-                                               w[7]);
-                        if (seed) {
-                            S.insert(gm);
-                        } else if (__any_sync(0xffffffffu, gm <= T0)) {
-                            const int col = cb + 32 * c + 8 * g;
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const int room = ln < a.CV ? 1 : 0;
+                            for (int e = 0; e < 8; ++e)
                                 asm volatile(
-                                    "{\n\t.reg .pred p, q;\n\t"
-                                    "setp.le.f32 p, %0, %1;\n\t"
-                                    "setp.ne.and.s32 q, %2, 0, p;\n\t"
-                                    "@q st.global.v2.b32 [%3], {%0, %4};\n\t}" ::"f"(w[e]),
-                                    "f"(T0), "r"(room), "l"(vlp), "r"(col + e)
+                                    "{\n\t.reg .pred p;\n\t"
+                                    "setp.le.f32 p, %1, %2;\n\t"
+                                    "@p st.global.v2.b32 [%0], {%1, %3};\n\t"
+                                    "@p add.s64 %0, %0, 8;\n\t}"
+                                    : "+l"(vlp)
+                                    : "f"(w[e]), "f"(T0), "r"(col + e)
                                     : "memory");
-                                const int hit = w[e] <= T0 ? 1 : 0;
-                                vlp += hit;
-                                ln += hit;
-                            }
+                            ln += static_cast<int>(vlp - v0);
+                            continue;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int room = ln < a.CV ? 1 : 0;
+                            asm volatile(
+                                "{\n\t.reg .pred p, q;\n\t"
+                                "setp.le.f32 p, %0, %1;\n\t"
+                                "setp.ne.and.s32 q, %2, 0, p;\n\t"
+                                "@q st.global.v2.b32 [%3], {%0, %4};\n\t}" ::"f"(w[e]),
+                                "f"(T0), "r"(room), "l"(vlp), "r"(col + e)
+                                : "memory");
+                            const int hit = w[e] <= T0 ? 1 : 0;
+                            vlp += hit;
+                            ln += hit;
                         }
                     }
                 }
