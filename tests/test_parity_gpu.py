@@ -171,6 +171,24 @@ def test_paths_are_bitwise_identical(knn, oracle, k):
         assert (t.distance == tabs[0].distance).all()
 
 
+@pytest.mark.parametrize("metric", [EUCLIDEAN, MANHATTAN, CHEBYSHEV])
+def test_exact_kernel_work_split_and_list_variants(knn, oracle, metric):
+    """The exact SIMT kernel's stream-K split (a query block spread over many
+    CTAs, one output slot per CTA, padded slots) and its list variants
+    (register lists of 1/2/4 x 32 entries, global lists above 128), on ragged
+    d (zero-filled coordinate tails) and partial last tiles."""
+    cases = [(100, 20011, 33, 32), (100, 20011, 33, 33), (7, 9000, 1, 64), (129, 5000, 97, 65),
+             (300, 3000, 31, 128), (60, 4100, 12, 129), (257, 700, 5, 1)]
+    for (n, m, d, k) in cases:
+        Q = oracle.uniform_f32(n, d, 300 + n) * 4 - 2
+        R = oracle.uniform_f32(m, d, 400 + m) * 4 - 2
+        ri, rd = oracle.knn(Q, R, k, metric)
+        t = knn.bf_knn(Q, R, k, knn.Metric(metric), config=cfg(knn, "exact"))
+        rep = compare(t.index, t.distance, ri, rd, Q, R, metric, oracle=oracle)
+        assert rep.ok, f"{(n, m, d, k)} metric={metric}: {rep}"
+        check_invariants(t, m)
+
+
 def test_chunk_and_workers_do_not_change_results(knn, oracle):
     # test_bruteforce.cpp:124-136
     R = oracle.uniform_f32(53, 6, 102)
