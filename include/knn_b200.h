@@ -107,7 +107,9 @@ KNN_B200_API knn_b200_status knn_b200_search(const float *queries, int64_t n, in
 
 /* Same search on DEVICE buffers (inputs already resident in HBM).  Runs on
  * opt->stream (or the engine stream) and returns without synchronizing when
- * a stream is given.  Mahalanobis is not accepted here (whiten first). */
+ * a stream is given.  Mahalanobis (opt->mahalanobis, d <= 8192): the inputs
+ * are whitened on the device into engine scratch copies (the caller's buffers
+ * are not modified), bitwise as the host path does. */
 KNN_B200_API knn_b200_status knn_b200_search_device(const float *d_queries, int64_t n,
                                        const float *d_references, int64_t m, int32_t d,
                                        int32_t k, int32_t metric,

@@ -283,10 +283,18 @@ def bf_knn(queries, references, k: int, metric: Metric = None, config: BfConfig 
 
 def search_device(q_ptr: int, n: int, r_ptr: int, m: int, d: int, k: int, out_dist_ptr: int,
                   out_idx_ptr: int, metric: int = EUCLIDEAN, path: int = PATH_AUTO,
-                  stream: int = 0, raw_keys: bool = False, device: int = -1) -> None:
-    """Device-resident search on raw device pointers (e.g. ``tensor.data_ptr()``)."""
+                  stream: int = 0, raw_keys: bool = False, device: int = -1,
+                  mahalanobis=None) -> None:
+    """Device-resident search on raw device pointers (e.g. ``tensor.data_ptr()``).
+    ``mahalanobis``: the d x d matrix when ``metric`` is MAHALANOBIS (the
+    inputs are whitened on the device into scratch copies)."""
     cfg = BfConfig(path=path, device=device)
     o = _opts(cfg, raw_keys=raw_keys, stream=stream)
+    keep = None
+    if mahalanobis is not None:
+        keep = np.ascontiguousarray(mahalanobis, np.float64)
+        o.mahalanobis = keep.ctypes.data
+        o.mahalanobis_dim = int(round(keep.size ** 0.5))
     _check(library().knn_b200_search_device(q_ptr, n, r_ptr, m, d, k, metric, C.byref(o),
                                             out_dist_ptr, out_idx_ptr))
 

@@ -8,9 +8,11 @@
 //   Metric::check_compatible ..... include/knn/metric.hpp:90-96
 // Invalid arguments map to KNN_B200_EINVAL with that text in
 // knn_b200_last_error(); the C++ mirror rethrows them as std::invalid_argument.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/knn_b200.h"
@@ -144,6 +146,50 @@ std::vector<float> whiten(const std::vector<double>& L, const float* x, int64_t 
     return out;
 }
 
+// Device whitening, bitwise equal to whiten(): y_r = sum_{c >= r} L[c][r] x_c
+// with round-to-nearest double multiplies and adds in ascending c, narrowed to
+// FP32.  In place: a block stages each point's row (as double) in shared
+// memory before overwriting it.  LT = L^T row-major (LT[r][c] = L[c][r]).
+constexpr int kWhitenMaxD = 8192;  // row staging: d doubles of shared memory
+
+__global__ void __launch_bounds__(128) whiten_kernel(float* X, int64_t n, int d, const double* LT) {
+    extern __shared__ double xs[];
+    for (int64_t p = blockIdx.x; p < n; p += gridDim.x) {
+        float* row = X + p * d;
+        for (int c = threadIdx.x; c < d; c += blockDim.x) xs[c] = static_cast<double>(row[c]);
+        __syncthreads();
+        for (int r = threadIdx.x; r < d; r += blockDim.x) {
+            const double* lt = LT + static_cast<int64_t>(r) * d;
+            double acc = 0.0;
+            for (int c = r; c < d; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(lt + c), xs[c]));
+            row[r] = __double2float_rn(acc);
+        }
+        __syncthreads();
+    }
+}
+
+// Whiten device rows in place (Q and R of one search) with the Cholesky factor
+// L (host, d x d row-major); dLT: device scratch of d*d doubles.
+void whiten_device(cudaStream_t s, const std::vector<double>& L, int d, double* dLT, float* X1,
+                   int64_t n1, float* X2, int64_t n2) {
+    std::vector<double> LT(static_cast<size_t>(d) * d);
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) LT[static_cast<size_t>(r) * d + c] = L[static_cast<size_t>(c) * d + r];
+    KNN_CUDA_CHECK(cudaMemcpyAsync(dLT, LT.data(), sizeof(double) * LT.size(), cudaMemcpyHostToDevice, s));
+    const size_t smem = sizeof(double) * d;
+    if (smem > 48 * 1024)
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(whiten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+    for (auto [X, n] : {std::pair<float*, int64_t>{X1, n1}, std::pair<float*, int64_t>{X2, n2}}) {
+        if (n == 0) continue;
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n, 148 * 16));
+        whiten_kernel<<<grid, 128, smem, s>>>(X, n, d, dLT);
+        KNN_LAUNCH_CHECK();
+    }
+    // the host copy of LT must outlive the async copy
+    KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
 // bruteforce.cpp:44-56 in order, then Metric::check_compatible.
 void check_search(int64_t dq, int64_t dr, int64_t m, int64_t k, const knn_b200_options& o,
                   int metric) {
@@ -219,7 +265,7 @@ unsigned scan_grid(int64_t count) {
 // One-shot host search, staged: H2D of both sets, device value check, search, D2H.
 void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r, int64_t m,
                    int dq, int dr, int k, int metric, int path, int raw_keys, bool host_values,
-                   float* out_dist, int64_t* out_idx) {
+                   float* out_dist, int64_t* out_idx, const std::vector<double>* chol = nullptr) {
     cudaStream_t s = ctx.stream;
     Sizer sz;
     sz.take<float>(static_cast<size_t>(n) * dq);
@@ -227,6 +273,7 @@ void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r
     sz.take<float>(static_cast<size_t>(n) * k);
     sz.take<int64_t>(static_cast<size_t>(n) * k);
     sz.take<unsigned long long>(2);
+    if (chol) sz.take<double>(static_cast<size_t>(dq) * dq);
     ctx.io.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.io.base())};
     float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
@@ -236,6 +283,10 @@ void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r
     unsigned long long* dbad = cv.take<unsigned long long>(2);
     KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, q, sizeof(float) * n * dq, cudaMemcpyHostToDevice, s));
     KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * dr, cudaMemcpyHostToDevice, s));
+    if (chol) {  // Mahalanobis: whiten on the device, then the Euclidean kernel
+        double* dLT = cv.take<double>(static_cast<size_t>(dq) * dq);
+        whiten_device(s, *chol, dq, dLT, dQ, n, dR, m);
+    }
     if (!host_values) {
         KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
         finite_scan_kernel<<<scan_grid(n * dq), 256, 0, s>>>(dQ, n * dq, dbad);
@@ -401,12 +452,16 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         const float* q = queries;
         const float* r = references;
         int kernel_metric = metric;
+        bool device_whiten = false;
         if (metric == kMahalanobis) {
-            wq = whiten(chol, queries, n, dq);
-            wr = whiten(chol, references, m, dr);
-            q = wq.data();
-            r = wr.data();
             kernel_metric = kL2;
+            device_whiten = device_present() && dq <= kWhitenMaxD;
+            if (!device_whiten) {  // the reference's own host step (metric.cpp:63-82)
+                wq = whiten(chol, queries, n, dq);
+                wr = whiten(chol, references, m, dr);
+                q = wq.data();
+                r = wr.data();
+            }
         }
 
         DeviceContext& ctx = context_for(o.device);
@@ -417,7 +472,7 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
             search_pipelined(ctx, q, n, r, m, dq, k, o.raw_keys, out_dist, out_idx);
         else
             search_staged(ctx, q, n, r, m, dq, dr, k, kernel_metric, o.path, o.raw_keys, host_values,
-                          out_dist, out_idx);
+                          out_dist, out_idx, device_whiten ? &chol : nullptr);
         if (distance_evals)
             *distance_evals = o.count_distance_evals ? static_cast<uint64_t>(n) * m : 0;
     });
@@ -430,18 +485,41 @@ knn_b200_status knn_b200_search_device(const float* d_queries, int64_t n,
     return guarded([&] {
         knn_b200_options tmp;
         const knn_b200_options& o = opts_or_default(opt, tmp);
-        if (metric == kMahalanobis)
-            throw InvalidArgument("knn_b200_search_device: whiten inputs for Mahalanobis");
+        std::vector<double> chol;
+        if (metric == kMahalanobis) chol = cholesky_or_throw(o.mahalanobis, o.mahalanobis_dim);
         check_point_set(d_queries, n, d, false);
         check_point_set(d_references, m, d, false);
         check_search(d, d, m, k, o, metric);
         if (!d_out_dist || !d_out_idx) throw InvalidArgument("bf_knn: null output pointer");
+        if (metric == kMahalanobis && d > kWhitenMaxD)
+            throw InvalidArgument("knn_b200_search_device: Mahalanobis needs d <= " +
+                                  std::to_string(kWhitenMaxD));
         DeviceContext& ctx = context_for(o.device);
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
-        search_device(ctx, s, d_queries, n, d_references, m, d, k, metric, o.path, o.raw_keys, 0,
-                      d_out_dist, d_out_idx);
+        const float* q = d_queries;
+        const float* r = d_references;
+        int kernel_metric = metric;
+        if (metric == kMahalanobis) {  // whitened copies (the inputs are the caller's)
+            Sizer sz;
+            sz.take<float>(static_cast<size_t>(n) * d);
+            sz.take<float>(static_cast<size_t>(m) * d);
+            sz.take<double>(static_cast<size_t>(d) * d);
+            ctx.io.reserve(sz.used + 256);
+            Carver cv{static_cast<char*>(ctx.io.base())};
+            float* wq = cv.take<float>(static_cast<size_t>(n) * d);
+            float* wr = cv.take<float>(static_cast<size_t>(m) * d);
+            double* dLT = cv.take<double>(static_cast<size_t>(d) * d);
+            KNN_CUDA_CHECK(cudaMemcpyAsync(wq, q, sizeof(float) * n * d, cudaMemcpyDeviceToDevice, s));
+            KNN_CUDA_CHECK(cudaMemcpyAsync(wr, r, sizeof(float) * m * d, cudaMemcpyDeviceToDevice, s));
+            whiten_device(s, chol, d, dLT, wq, n, wr, m);
+            q = wq;
+            r = wr;
+            kernel_metric = kL2;
+        }
+        search_device(ctx, s, q, n, r, m, d, k, kernel_metric, o.path, o.raw_keys, 0, d_out_dist,
+                      d_out_idx);
         if (!o.stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }

@@ -189,6 +189,35 @@ def test_exact_kernel_work_split_and_list_variants(knn, oracle, metric):
         check_invariants(t, m)
 
 
+def test_mahalanobis_device_whitening(knn, oracle):
+    """Metric::whiten (metric.cpp:63-82) runs on the device for both the host
+    and the device-resident API; both equal the oracle within tolerance and
+    each other bitwise."""
+    import torch
+    rng = np.random.default_rng(77)
+    d = 24
+    A = rng.standard_normal((d, d))
+    M = A @ A.T + d * np.eye(d)
+    Q = (rng.random((300, d)) * 4 - 2).astype(np.float32)
+    R = (rng.random((5000, d)) * 4 - 2).astype(np.float32)
+    k = 15
+    ri, rd = oracle.knn(Q, R, k, MAHALANOBIS, M.ravel())
+    th = knn.bf_knn(Q, R, k, knn.Metric.mahalanobis(d, M.ravel()))
+    rep = compare(th.index, th.distance, ri, rd, Q, R, MAHALANOBIS, oracle=oracle,
+                  mahal=M.ravel(), atol=1e-6)
+    assert rep.ok, str(rep)
+    Qd = torch.from_numpy(Q).cuda()
+    Rd = torch.from_numpy(R).cuda()
+    od = torch.empty((300, k), device="cuda")
+    oi = torch.empty((300, k), dtype=torch.int64, device="cuda")
+    knn.search_device(Qd.data_ptr(), 300, Rd.data_ptr(), 5000, d, k, od.data_ptr(), oi.data_ptr(),
+                      metric=MAHALANOBIS, mahalanobis=M)
+    torch.cuda.synchronize()
+    assert (oi.cpu().numpy() == th.index).all()
+    assert (od.cpu().numpy() == th.distance).all()
+    assert (Qd.cpu().numpy() == Q).all()  # caller's inputs untouched
+
+
 def test_chunk_and_workers_do_not_change_results(knn, oracle):
     # test_bruteforce.cpp:124-136
     R = oracle.uniform_f32(53, 6, 102)
