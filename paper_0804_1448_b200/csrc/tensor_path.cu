@@ -76,6 +76,19 @@ __device__ __forceinline__ float thresh(float ak, const Consts& c) {
     return t + fabsf(t) * 4e-6f + 1e-30f;
 }
 
+// Stream-K unit split of the filter: CTA c owns units [U c / G, U (c+1) / G)
+// of the (query-tile pair, reference tile) sequence.
+__device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
+    return (U * c) / G;
+}
+
+__device__ __forceinline__ int first_cta_of(int64_t u0, int64_t U, int G) {
+    int c = static_cast<int>((u0 * G) / U);
+    while (c + 1 < G && unit_start(U, G, c + 1) <= u0) ++c;
+    while (c > 0 && unit_start(U, G, c) > u0) --c;
+    return c;
+}
+
 struct PrepArgs {
     const float* X;     // rows x d
     int64_t rows, rows_pad;
@@ -89,6 +102,9 @@ struct PrepArgs {
     unsigned* gmax;     // refs: [0] max delta_r bits, [1] max ||r~|| bits
     unsigned* tinit;    // queries: per-row cross-CTA bound, set to "none" (0xffffffff)
     int* zero;          // queries: a counter cleared by block 0 (fallback count)
+    int* pair_slots;    // queries: per query-tile pair, the number of CTAs touching it
+    int pairs, G, rtiles;
+    int64_t U;
 };
 
 // ordered-uint encoding of floats for atomicMin/Max over signed values
@@ -202,6 +218,12 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
     const int wib = threadIdx.x >> 5;
     const float s = *a.scale;
     if (QUERY && a.zero && blockIdx.x == 0 && threadIdx.x == 0) *a.zero = 0;
+    if (QUERY && a.pair_slots)
+        for (int p = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x); p < a.pairs;
+             p += static_cast<int>(gridDim.x * blockDim.x)) {
+            const int64_t u0 = static_cast<int64_t>(p) * a.rtiles;
+            a.pair_slots[p] = first_cta_of(u0 + a.rtiles - 1, a.U, a.G) - first_cta_of(u0, a.U, a.G) + 1;
+        }
     // reference sets: running maxima of the rounding radius and of ||r~||,
     // reduced per block (one global atomic per block, not per row)
     float dmax = 0.f, nmax = 0.f;
@@ -323,18 +345,8 @@ struct FilterArgs {
     float* t0;             // [n_pad]
     float2* vlog;          // [parts][128][CV]
     int CV;
+    const int* pair_slots;  // [pairs] CTAs touching each query-tile pair (query prep)
 };
-
-__device__ __forceinline__ int64_t unit_start(int64_t U, int G, int c) {
-    return (U * c) / G;
-}
-
-__device__ __forceinline__ int first_cta_of(int64_t u0, int64_t U, int G) {
-    int c = static_cast<int>((u0 * G) / U);
-    while (c + 1 < G && unit_start(U, G, c + 1) <= u0) ++c;
-    while (c > 0 && unit_start(U, G, c) > u0) --c;
-    return c;
-}
 
 __device__ __forceinline__ Consts load_consts(const FilterArgs& a, int64_t q) {
     const float4 qc = a.qconst[q];
@@ -408,6 +420,44 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
     return v;
+}
+
+// 32-byte read-only global load (one full sector per lane: LDG.E.256)
+__device__ __forceinline__ void ldg8(const float* p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                   "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+// Exact FP32 key of one (query row, reference row) pair, key_step order.
+// Rows 32-byte aligned (d % 8 == 0, 32-byte aligned bases): 256-bit loads.
+__device__ __forceinline__ float exact_key_l2(const float* qrow, const float* rrow, int d) {
+    float acc = 0.f;
+    if ((d & 7) == 0 && ((reinterpret_cast<uintptr_t>(qrow) | reinterpret_cast<uintptr_t>(rrow)) & 31) == 0) {
+#pragma unroll 4
+        for (int c8 = 0; c8 < (d >> 3); ++c8) {
+            float u[8], w[8];
+            ldg8(qrow + 8 * c8, u);
+            ldg8(rrow + 8 * c8, w);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = key_step<kL2>(acc, u[e], w[e]);
+        }
+    } else if ((d & 3) == 0) {
+        const float4* q4 = reinterpret_cast<const float4*>(qrow);
+        const float4* r4 = reinterpret_cast<const float4*>(rrow);
+#pragma unroll 8
+        for (int c4 = 0; c4 < (d >> 2); ++c4) {
+            const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
+            acc = key_step<kL2>(acc, u.x, w.x);
+            acc = key_step<kL2>(acc, u.y, w.y);
+            acc = key_step<kL2>(acc, u.z, w.z);
+            acc = key_step<kL2>(acc, u.w, w.w);
+        }
+    } else {
+        for (int cc = 0; cc < d; ++cc) acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
+    }
+    return acc;
 }
 
 // The KR smallest group minima seen by this (query, CTA part), sorted
@@ -1255,9 +1305,7 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
         int off = 0;
         bool over = false;
         const int pair = qt >> 1;  // slots written: one per CTA touching the pair
-        const int nslots = first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles + a.f.rtiles - 1,
-                                        a.f.U, a.f.G) -
-                           first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles, a.f.U, a.f.G) + 1;
+        const int nslots = a.f.pair_slots[pair];
         for (int p = 0; p < a.S_max; ++p) {
             const int np = p < nslots ? a.f.log_n[(p0 + p) * TILE + row] : 0;
             over |= np > a.f.CV;
@@ -1317,25 +1365,8 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
     }
     // exact keys of the nc candidates (their indices are si[0..nc))
     const float* qrow = a.Q + q * a.d;
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-        const float* rrow = a.R + static_cast<int64_t>(si[c]) * a.d;
-        float acc = 0.f;
-        if ((a.d & 3) == 0) {
-            const float4* q4 = reinterpret_cast<const float4*>(qrow);
-            const float4* r4 = reinterpret_cast<const float4*>(rrow);
-#pragma unroll 4
-            for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
-                const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
-                acc = key_step<kL2>(acc, u.x, w.x);
-                acc = key_step<kL2>(acc, u.y, w.y);
-                acc = key_step<kL2>(acc, u.z, w.z);
-                acc = key_step<kL2>(acc, u.w, w.w);
-            }
-        } else {
-            for (int cc = 0; cc < a.d; ++cc) acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
-        }
-        sk[c] = acc;
-    }
+    for (int c = threadIdx.x; c < nc; c += blockDim.x)
+        sk[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(si[c]) * a.d, a.d);
     int N2 = 32;
     while (N2 < nc) N2 <<= 1;
     for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
@@ -1429,9 +1460,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     // memory round trip per step): the kernel is latency-bound per warp.
     // part slots written for this pair: one per CTA whose unit range touches it
     const int pair = qt >> 1;
-    const int nslots = first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles + a.f.rtiles - 1, a.f.U,
-                                    a.f.G) -
-                       first_cta_of(static_cast<int64_t>(pair) * a.f.rtiles, a.f.U, a.f.G) + 1;
+    const int nslots = a.f.pair_slots[pair];
     int cnt = 0, nlog = 0;
     if (lane < nslots) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
@@ -1446,26 +1475,40 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         if (lane >= o) cincl += y;
     }
     const int L = __shfl_sync(0xffffffffu, cincl, 31);
-    for (int x0 = 0; x0 < span; x0 += 32) {
-        const int x = x0 + lane;
-        const int p = x / Kq, e = x - p * Kq;
-        const int cp = __shfl_sync(0xffffffffu, cnt, p & 31);
-        const int ep = __shfl_sync(0xffffffffu, cincl, p & 31) - cp;
-        if (x < span && e < cp) sv[ep + e] = a.f.part_A[((p0 + p) * Kq + e) * TILE + row];
+    for (int p = 0; p < nslots; ++p) {  // a list holds <= Kq <= 32 entries
+        const int cp = __shfl_sync(0xffffffffu, cnt, p);
+        const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+        if (lane < cp) sv[ep + lane] = a.f.part_A[((p0 + p) * Kq + lane) * TILE + row];
     }
     __syncwarp();
 
-    // 1. k-th smallest (value, position) of the compacted lists
+    // 1. k-th smallest (value, position) of the compacted lists.  Each list is
+    //    sorted, so an entry's rank is its own position plus, per other list,
+    //    a binary search: entries <= v of earlier lists, < v of later ones.
     float B = kInf;
     if (L >= k) {
-        for (int x = lane; x < L; x += 32) {
-            const float v = sv[x];
-            int c = 0;
-            for (int y = 0; y < L; ++y) {
-                const float w = sv[y];
-                c += (w < v || (w == v && y < x)) ? 1 : 0;
+        for (int x0 = 0; x0 < L; x0 += 32) {  // warp-uniform trip count (shuffles inside)
+            const int x = x0 + lane;
+            const bool valid = x < L;
+            const float v = valid ? sv[x] : kInf;
+            int px = 0;
+            for (int p = 1; p < nslots; ++p)
+                if (x >= __shfl_sync(0xffffffffu, cincl, p - 1)) px = p;
+            int rank = 0;
+            for (int p = 0; p < nslots; ++p) {
+                const int cp = __shfl_sync(0xffffffffu, cnt, p);
+                const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+                // first entry of list p that is not "less" than (v, x)
+                int lo = 0, hi = (p == px || !valid) ? 0 : cp;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const float w = sv[ep + mid];
+                    if (p < px ? w <= v : w < v) lo = mid + 1;
+                    else hi = mid;
+                }
+                rank += p == px ? x - ep : lo;
             }
-            if (c == k - 1) B = v;
+            if (valid && rank == k - 1) B = v;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
@@ -1480,35 +1523,19 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     //    minimum is inside tau, then their values <= tau.
     int nc = 0;
     if (ok) {
-        int incl = nlog;  // inclusive prefix of the log lengths over parts
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
         int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
         int ng = 0;
-        for (int t0 = 0; t0 < total; t0 += 32) {
-            const int t = t0 + lane;
-            int p = 0, before = 0;  // part holding flattened group t, groups before it
-            for (int pp = 0; pp < parts; ++pp) {
-                const int ip = __shfl_sync(0xffffffffu, incl, pp);
-                if (t >= ip) {
-                    p = pp + 1;
-                    before = ip;
-                }
+        for (int p = 0; p < nslots; ++p) {
+            const int np = __shfl_sync(0xffffffffu, nlog, p);
+            const int base = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG);
+            for (int t0 = 0; t0 < np; t0 += 32) {
+                const int t = t0 + lane;
+                const bool in = t < np && __int_as_float(a.f.log_h[base + t].x) <= tau;
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pos = ng + __popc(bal & ((1u << lane) - 1u));
+                if (in && pos < RR_CAND) gl[pos] = base + t;
+                ng += __popc(bal);
             }
-            int slot = -1;
-            bool in = false;
-            if (t < total) {
-                slot = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG + (t - before));
-                in = __int_as_float(a.f.log_h[slot].x) <= tau;
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, in);
-            const int pos = ng + __popc(bal & ((1u << lane) - 1u));
-            if (in && pos < RR_CAND) gl[pos] = slot;
-            ng += __popc(bal);
         }
         ok = ng <= RR_CAND;
         __syncwarp();
@@ -1549,36 +1576,41 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
 
     // 4. exact FP32 keys of the candidates (lane-parallel, fixed coordinate order)
     const float* qrow = a.Q + q * a.d;
-    for (int c = lane; c < nc; c += 32) {
-        const float* rrow = a.R + static_cast<int64_t>(ci[c]) * a.d;
-        float acc = 0.f;
-        if ((a.d & 3) == 0) {
-            const float4* q4 = reinterpret_cast<const float4*>(qrow);
-            const float4* r4 = reinterpret_cast<const float4*>(rrow);
-#pragma unroll 8
-            for (int c4 = 0; c4 < (a.d >> 2); ++c4) {
-                const float4 u = __ldg(q4 + c4), w = __ldg(r4 + c4);
-                acc = key_step<kL2>(acc, u.x, w.x);
-                acc = key_step<kL2>(acc, u.y, w.y);
-                acc = key_step<kL2>(acc, u.z, w.z);
-                acc = key_step<kL2>(acc, u.w, w.w);
-            }
-        } else {
-            for (int cc = 0; cc < a.d; ++cc) acc = key_step<kL2>(acc, __ldg(qrow + cc), __ldg(rrow + cc));
-        }
-        ck[c] = acc;
-    }
+    for (int c = lane; c < nc; c += 32)
+        ck[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(ci[c]) * a.d, a.d);
     __syncwarp();
 
-    // 5. exact top-k: rank of every candidate under the (key, index) order
-    for (int c = lane; c < nc; c += 32) {
-        const float kc = ck[c];
-        const int jc = ci[c];
-        int r = 0;
-        for (int c2 = 0; c2 < nc; ++c2) r += pair_less(ck[c2], ci[c2], kc, jc) ? 1 : 0;
-        if (r < k) {
-            fk[r] = kc;
-            fi[r] = jc;
+    // 5. exact top-k under the (key, index) order: up to 32 candidates, one
+    //    per lane, by a shuffle bitonic network; more, by rank counting
+    if (nc <= 32) {
+        float kc = lane < nc ? ck[lane] : kInf;
+        int jc = lane < nc ? ci[lane] : 0x7fffffff;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float pk = __shfl_xor_sync(0xffffffffu, kc, stride);
+                const int pj = __shfl_xor_sync(0xffffffffu, jc, stride);
+                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                if (pair_less(pk, pj, kc, jc) == keep_min) {
+                    kc = pk;
+                    jc = pj;
+                }
+            }
+        if (lane < k) {
+            fk[lane] = kc;
+            fi[lane] = jc;
+        }
+    } else {
+        for (int c = lane; c < nc; c += 32) {
+            const float kc = ck[c];
+            const int jc = ci[c];
+            int r = 0;
+            for (int c2 = 0; c2 < nc; ++c2) r += pair_less(ck[c2], ci[c2], kc, jc) ? 1 : 0;
+            if (r < k) {
+                fk[r] = kc;
+                fi[r] = jc;
+            }
         }
     }
     __syncwarp();
@@ -1801,6 +1833,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     sz.take<unsigned>(static_cast<size_t>(n_pad));
     sz.take<float>(large ? static_cast<size_t>(n_pad) : 0);
     sz.take<float2>(static_cast<size_t>(parts) * TILE * CV);
+    sz.take<int>(static_cast<size_t>(pairs));
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -1816,6 +1849,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     unsigned* tglob = cv.take<unsigned>(static_cast<size_t>(n_pad));
     float* t0 = cv.take<float>(large ? static_cast<size_t>(n_pad) : 0);
     float2* vlog = cv.take<float2>(static_cast<size_t>(parts) * TILE * CV);
+    int* pair_slots = cv.take<int>(static_cast<size_t>(pairs));
     const unsigned* gmax = refs.gmax;
 
     // 1. per-search state and the query-side prep
@@ -1836,6 +1870,11 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     pr.qconst = qconst;
     pr.tinit = tglob;
     pr.zero = fb;
+    pr.pair_slots = pair_slots;
+    pr.pairs = pairs;
+    pr.G = G;
+    pr.rtiles = rtiles;
+    pr.U = U;
     {
         ProfileScope ps(stream, "prep_convert_queries");
         convert_kernel<true><<<static_cast<unsigned>(std::min<int64_t>((n_pad + 7) / 8, 8 * kSmCount)),
@@ -1873,6 +1912,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     fa.log_n = log_n;
     fa.log_v = log_v;
     fa.log_h = log_h;
+    fa.pair_slots = pair_slots;
     fa.CG = CG;
     if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
     fa.drain_at = 8;
