@@ -403,6 +403,31 @@ __device__ __forceinline__ void push_group(float gm, float tf, uint32_t sg, int 
         : "memory");
 }
 
+// push_group with the bookkeeping folded into the predicates: `off` counts the
+// groups logged by this (query, part) including overflow (slot = off), `sgp`
+// is the next smem buffer slot; both advance only on a hit.
+template <int STRIDE>
+__device__ __forceinline__ void push_group_off(float gm, float tf, uint32_t& sgp, int& off, int cg,
+                                               const float4* lvb, const int2* lhb, const float* w,
+                                               int col) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .u64 a, b;\n\t"
+        "setp.le.f32 p, %2, %3;\n\t"
+        "setp.lt.and.s32 q, %1, %4, p;\n\t"
+        "@p st.shared.f32 [%0], %2;\n\t"
+        "mad.wide.s32 a, %1, 32, %5;\n\t"
+        "mad.wide.s32 b, %1, 8, %6;\n\t"
+        "@q st.global.v4.f32 [a], {%8, %9, %10, %11};\n\t"
+        "@q st.global.v4.f32 [a+16], {%12, %13, %14, %15};\n\t"
+        "@q st.global.v2.b32 [b], {%2, %7};\n\t"
+        "@p add.s32 %1, %1, 1;\n\t"
+        "@p add.s32 %0, %0, %16;\n\t}"
+        : "+r"(sgp), "+r"(off)
+        : "f"(gm), "f"(tf), "r"(cg), "l"(lvb), "l"(lhb), "r"(col), "f"(w[0]), "f"(w[1]), "f"(w[2]),
+          "f"(w[3]), "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "n"(STRIDE)
+        : "memory");
+}
+
 // no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~
 __device__ __forceinline__ void add_rnorm(float (&v)[32], const float* rn) {
     const float4* nr = reinterpret_cast<const float4*>(rn);
@@ -700,15 +725,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         RegList<KR> L;
         L.reset();
         int cur_p = -1;
-        int nb = 0;        // buffered group minima
+        uint32_t sgp = sg0;  // next buffer slot: (sgp - sg0) / (4 EPI_THREADS) minima buffered
         float T = kInf;    // own bound: thresh(k-th smallest group minimum of this list)
         float Tf = kInf;   // filter bound: min over every valid bound for this query
         unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
         Consts qc{};
         int64_t q = 0;
         int64_t part = 0;
-        float4* lvp = nullptr;  // next slot of this (query, part)'s group log
-        int2* lhp = nullptr;
+        const float4* lvb = nullptr;  // this (query, part)'s group log
+        const int2* lhb = nullptr;
         int ln = 0;            // groups logged so far (may exceed CG: overflow)
         unsigned long long st_drains = 0, st_rounds = 0;
         long long st_cyc_drain = 0, st_cyc_wait = 0;
@@ -723,13 +748,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     do {                                                                                         \
         const long long c0_ = (kStats && a.stats) ? clock64() : 0;                                           \
         if (kStats && a.stats) ++st_drains;                                                                \
+        const int nb = static_cast<int>((sgp - sg0) / (EPI_THREADS * 4));                       \
         const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
         _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
             if (kStats && a.stats) ++st_rounds;                                                            \
             const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
             if (g_ <= Tf) L.insert(g_);                                                          \
         }                                                                                        \
-        nb = 0;                                                                                  \
+        sgp = sg0;                                                                               \
         if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
         float tf_ = fminf(T, dec_or_inf(tg_pref));                                               \
         if (T < kInf) atomicMin(a.tglob + q, enc(T));                                            \
@@ -763,15 +789,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             any_ |= gm_[i_] <= Tf;                                                               \
         }                                                                                        \
         if (a.mode != 3 && __any_sync(0xffffffffu, any_)) { /* some lane pushes: most chunks */ \
-            _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                   \
-                push_group(gm_[i_], Tf, sg0 + static_cast<uint32_t>(nb) * (EPI_THREADS * 4),     \
-                           ln < a.CG ? 1 : 0, lvp, lhp, vv + 8 * i_, (colb) + 8 * i_);           \
-                const int hit_ = gm_[i_] <= Tf ? 1 : 0;                                          \
-                nb += hit_;                                                                      \
-                ln += hit_;                                                                      \
-                lvp += hit_ ? 2 : 0;                                                             \
-                lhp += hit_;                                                                     \
-            }                                                                                    \
+            _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_)                                     \
+                push_group_off<EPI_THREADS * 4>(gm_[i_], Tf, sgp, ln, a.CG, lvb, lhb, vv + 8 * i_, \
+                                                (colb) + 8 * i_);                                \
         }                                                                                        \
     } while (0)
 
@@ -820,15 +840,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
                 part = static_cast<int64_t>(qt) * a.S_max + slot;
                 const int64_t lq = (part * TILE + row) * a.CG;
-                lvp = a.log_v + 2 * lq;
-                lhp = a.log_h + lq;
+                lvb = a.log_v + 2 * lq;
+                lhb = a.log_h + lq;
                 ln = 0;
                 qc = load_consts(a, q);
                 L.reset();
                 T = kInf;
                 tg_pref = __ldcg(a.tglob + q);
                 Tf = dec_or_inf(tg_pref);
-                nb = 0;
+                sgp = sg0;
             }
             const int col_base = rt * TILE;
             const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
@@ -848,7 +868,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 release(t);  // all four chunks of tile t are in registers
                 KNN_SCAN_REGS(rb, col_base + 96);
                 // drain after the release, so the MMA never waits on the list
-                if (__any_sync(0xffffffffu, nb >= a.drain_at)) KNN_DRAIN();
+                if (__any_sync(0xffffffffu, sgp - sg0 >= static_cast<uint32_t>(a.drain_at * EPI_THREADS * 4)))
+                    KNN_DRAIN();
                 if (t + 1 < nunits) {
                     wait_full(t + 1);
                     sm100::tmem_ld_32x32b_x32(tlane + static_cast<uint32_t>(((t + 1) & 1) * TILE), ra);
