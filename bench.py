@@ -11,7 +11,8 @@ ours (default)
     the per-shard top-k lists are all-gathered over NCCL and merged on device
     (SURVEY.md 8(e)); total work is fixed, so scaling is "strong".
     Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA
-    events on the launch stream with an L2 flush (256 MiB write) between
+    events on the launch stream with an L2 flush (256 MiB write, then a
+    256 MiB read that evicts the dirty lines) between
     steps; barrier + synchronize around the timed region; max over ranks.
     e2e: the same metric through the public host API (pinned host Q/R in,
     host results out, H2D/D2H inside the timed region).
@@ -182,8 +183,12 @@ def run_ours(args):
     cfg = dict(CONFIG_B)
     n, m, d, k = cfg["n"], cfg["m"], cfg["d"], cfg["k"]
     path = {"auto": knn.PATH_AUTO, "exact": knn.PATH_EXACT, "tensor": knn.PATH_TENSOR}[args.path]
+    # a dedicated (non-default) stream: the engine, the L2 flush, the step
+    # events and NCCL all order on it (handle 0 would mean "engine stream")
+    torch.cuda.set_stream(torch.cuda.Stream(dev))
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
+    assert sptr != 0
 
     # synthetic inputs, generated on the device (counter-based splitmix64)
     sr, sq = seeds(cfg)
@@ -217,6 +222,9 @@ def run_ours(args):
                              out_i.data_ptr(), stream=sptr)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # a second buffer read after the flush write evicts the flush's dirty lines,
+    # so their write-back lands before the step's start event, not inside it
+    clean = torch.ones(64 << 20, dtype=torch.float32, device=dev)
     clocks = ClockSampler(local)
     clocks.start()
     for _ in range(args.warmup):
@@ -234,6 +242,7 @@ def run_ours(args):
     t_lo = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
+        clean.sum()
         starts[i].record(stream)
         step()
         ends[i].record(stream)
@@ -302,7 +311,7 @@ def run_ours(args):
             "config": {"workload": "configs[1]: m=n=38400, d=96, k=20, euclidean",
                        "m": m, "n": n, "d": d, "k": k, "metric": "euclidean",
                        "parallelism": "single" if world == 1 else f"reference-sharded x{world}",
-                       "path": args.path, "l2": "flushed between timed steps (256 MiB write)",
+                       "path": args.path, "l2": "flushed between timed steps (256 MiB write, then a 256 MiB read that evicts the dirty lines)",
                        "inputs": "uniform [0,1) fp32, splitmix64 counter stream, "
                                  "seeds derive_seed(42,m,d,0)/(42,n,d,1)",
                        "vs_baseline_ref": "paper Table 1 BF-CUDA 8800 GTX, 878 q/s"},

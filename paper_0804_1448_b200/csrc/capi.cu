@@ -370,6 +370,7 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     if (bad[0] != ~0ull) throw_non_finite(bad[0], d);
     if (bad[1] != ~0ull) throw_non_finite(bad[1], d);
     ctx.last_fallbacks = fails;
+    ctx.fb_on_device = false;
     if (fails == 0) return;
     // uncertified queries: the full dispatch (large-k retry, exact) on their rows
     std::vector<int> list(static_cast<size_t>(fails));
@@ -642,7 +643,15 @@ void knn_b200_index_destroy(knn_b200_index* index) { delete index; }
 
 int knn_b200_last_fallback_count(int device) {
     try {
-        return context_for(device).last_fallbacks;
+        DeviceContext& ctx = context_for(device);
+        if (ctx.fb_on_device) {  // resolved on the device by the last search
+            int v = 0;
+            KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+            KNN_CUDA_CHECK(cudaDeviceSynchronize());
+            KNN_CUDA_CHECK(cudaMemcpy(&v, ctx.fb_dev, sizeof(int), cudaMemcpyDeviceToHost));
+            return v;
+        }
+        return ctx.last_fallbacks;
     } catch (...) {
         return -1;
     }

@@ -75,58 +75,39 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
     a.m = m;
     a.d = d;
     a.k = k;
+    a.ntiles = exact_ntiles(m);
     a.index_base = index_base;
-    exact_plan(a, !big_k);
-    const int parts = a.parts;
-
+    a.raw_keys = raw_keys;
+    a.out_key = d_out;
+    a.out_idx = d_idx;
+    const int max_ctas = exact_max_ctas(k, !big_k);
+    const size_t part = static_cast<size_t>(exact_slots(n, a.ntiles, max_ctas)) *
+                        exact_queries_per_cta() * k;
+    const size_t lists = static_cast<size_t>(max_ctas) * exact_queries_per_cta() * k;
     Sizer sz;
-    if (parts > 1) {
-        sz.take<float>(static_cast<size_t>(parts) * n * k);
-        sz.take<int64_t>(static_cast<size_t>(parts) * n * k);
-    }
-    const size_t lists = static_cast<size_t>(a.ctas) * exact_queries_per_cta() * k;
+    sz.take<float>(part);
+    sz.take<int64_t>(part);
     if (big_k) {
         sz.take<float>(lists);
         sz.take<int32_t>(lists);
     }
-    if (parts > 1 && static_cast<size_t>(k) > 1024) {
+    if (k > 2048) {
         sz.take<float>(static_cast<size_t>(n) * k);
         sz.take<int64_t>(static_cast<size_t>(n) * k);
     }
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
-    float* part_key = d_out;
-    int64_t* part_idx = d_idx;
-    if (parts > 1) {
-        part_key = cv.take<float>(static_cast<size_t>(parts) * n * k);
-        part_idx = cv.take<int64_t>(static_cast<size_t>(parts) * n * k);
-    }
+    a.part_key = cv.take<float>(part);
+    a.part_idx = cv.take<int64_t>(part);
     if (big_k) {
         a.glist_key = cv.take<float>(lists);
         a.glist_idx = cv.take<int32_t>(lists);
     }
-    a.out_key = part_key;
-    a.out_idx = part_idx;
-    a.finalize = (parts == 1 && !raw_keys) ? 1 : 0;
-    launch_exact(metric, a, stream);
-
-    if (parts > 1) {
-        MergeArgs mg{};
-        mg.part_key = part_key;
-        mg.part_idx = part_idx;
-        mg.parts = parts;
-        mg.n = n;
-        mg.k = k;
-        mg.metric = metric;
-        mg.finalize = raw_keys ? 0 : 1;
-        mg.out_key = d_out;
-        mg.out_idx = d_idx;
-        if (static_cast<size_t>(k) > 1024) {
-            mg.glist_key = cv.take<float>(static_cast<size_t>(n) * k);
-            mg.glist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
-        }
-        launch_merge(mg, stream);
+    if (k > 2048) {
+        a.mglist_key = cv.take<float>(static_cast<size_t>(n) * k);
+        a.mglist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
     }
+    launch_exact(metric, a, stream);
 }
 
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,

@@ -54,6 +54,8 @@ struct DeviceContext {
     DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
     std::mutex mu;           // one search at a time per context
     int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
+    int* fb_dev = nullptr;     // ... the same count, when resolved on the device
+    bool fb_on_device = false;
 };
 
 DeviceContext& context_for(int device);  // device < 0: current device

@@ -75,7 +75,7 @@ __device__ __forceinline__ float2 key_step2(float2 acc, float q, float2 r) {
 
 // KP: list entries per lane of the register-resident list (k <= 32 KP, lists in
 // shared memory), or 0 for lists in global memory (k > 128, WarpList).
-template <int M, int KP>
+template <int M, int KP, bool INDIRECT = false>
 __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
     constexpr bool SMEM_LISTS = KP > 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -104,11 +104,12 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
 
     // stream-K: this CTA owns units [u, u_end) of the (query block, tile)
     // sequence; each query block it touches is one segment with its own lists
-    const int64_t W = a.units;
-    const int64_t G = gridDim.x;
-    int64_t u = static_cast<int64_t>(blockIdx.x) * W / G;
-    const int64_t u_end = static_cast<int64_t>(blockIdx.x + 1) * W / G;
-    auto cta_of = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
+    const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
+    if (n_eff <= 0) return;
+    const ExactSplit sp = exact_split(n_eff, a.ntiles, gridDim.x);
+    if (blockIdx.x >= sp.G) return;
+    int64_t u = sp.start(blockIdx.x);
+    const int64_t u_end = sp.start(blockIdx.x + 1);
 
     int buf = 0;
     while (u < u_end) {
@@ -117,9 +118,8 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
         const int t_b = static_cast<int>(min(static_cast<int64_t>(a.ntiles), t_a + (u_end - u)));
         u += t_b - t_a;
         const int64_t q0 = b * QT;
-        const int64_t first = cta_of(b * a.ntiles);
-        const int part = static_cast<int>(blockIdx.x - first);
-        const int nparts = static_cast<int>(cta_of((b + 1) * a.ntiles - 1) - first + 1);
+        const bool single = sp.cta_of(b * a.ntiles) == sp.cta_of((b + 1) * a.ntiles - 1);
+        const size_t slot = static_cast<size_t>(blockIdx.x + b);
 
         // warp w owns rows 2w + h + 16 i (h < 2, i < 8): its 16 lists are private
         for (int i = 0; i < 8; ++i)
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
         // (pair-interleaved).  Load s of this thread covers Q row 8 s + warp,
         // coordinate lane, and R reference t0 + 8 s + rr, coordinate rc, where a
         // warp reads 128 contiguous bytes of Q and 2 x 64 bytes of R.
-        const int nq = static_cast<int>(min(static_cast<int64_t>(QT), a.n - q0));
+        const int nq = static_cast<int>(min(static_cast<int64_t>(QT), n_eff - q0));
         auto issue = [&](int tile, int chunk, int sb) {
             const int64_t t0 = static_cast<int64_t>(tile) * RT;
             const int nr = static_cast<int>(min(static_cast<int64_t>(RT), m - t0));
@@ -150,7 +150,13 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
             for (int s = 0; s < LOADS; ++s) {
                 const bool okq = okq_c && 8 * s + warp < nq;
                 const bool okr = okr_c && 8 * s + rr < nr;
-                cp_async4(dq, okq ? gq : a.Q, okq);
+                if constexpr (INDIRECT) {
+                    const float* src = okq ? a.Q + static_cast<int64_t>(a.qlist[q0 + 8 * s + warp]) * d + c0 + lane
+                                           : a.Q;
+                    cp_async4(dq, src, okq);
+                } else {
+                    cp_async4(dq, okq ? gq : a.Q, okq);
+                }
                 cp_async4(dr, okr ? gr : a.R, okr);
                 gq += 8 * static_cast<int64_t>(d);
                 gr += 8 * static_cast<int64_t>(d);
@@ -274,30 +280,26 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
         }
         __syncwarp();
 
-        // emit this warp's lists into output slot `part` (raw keys for the
-        // merge, or finalized when every query block is one segment); the
-        // block's first CTA pads the slots its block does not use
+        // emit this warp's lists: final rows when this segment is the block's
+        // only one, else raw keys into the segment's slot for merge_exact
         for (int i = 0; i < 8; ++i)
             for (int h = 0; h < 2; ++h) {
                 const int row = 2 * warp + h + 16 * i;
                 const int64_t q = q0 + row;
-                if (q >= a.n) continue;
-                const size_t base = (static_cast<size_t>(part) * a.n + q) * a.k;
-                if (a.finalize) finalize_list(Lk + row * a.k, Li + row * a.k, a.k, M, lane);
-                for (int t = lane; t < a.k; t += 32) {
-                    const float key = Lk[row * a.k + t];
-                    const int32_t li = Li[row * a.k + t];
-                    a.out_key[base + t] = key;
-                    a.out_idx[base + t] = li == 0x7fffffff ? kSentinelIdx : a.index_base + li;
+                if (q >= n_eff) continue;
+                float* ok_ = a.part_key + (slot * QT + row) * a.k;
+                int64_t* oi_ = a.part_idx + (slot * QT + row) * a.k;
+                if (single) {
+                    const int64_t orow = INDIRECT ? static_cast<int64_t>(a.qlist[q]) : q;
+                    ok_ = a.out_key + orow * a.k;
+                    oi_ = a.out_idx + orow * a.k;
+                    if (!a.raw_keys) finalize_list(Lk + row * a.k, Li + row * a.k, a.k, M, lane);
                 }
-                if (part == 0)
-                    for (int pp = nparts; pp < a.parts; ++pp) {
-                        const size_t pb = (static_cast<size_t>(pp) * a.n + q) * a.k;
-                        for (int t = lane; t < a.k; t += 32) {
-                            a.out_key[pb + t] = kInf;
-                            a.out_idx[pb + t] = kSentinelIdx;
-                        }
-                    }
+                for (int t = lane; t < a.k; t += 32) {
+                    const int32_t li = Li[row * a.k + t];
+                    ok_[t] = Lk[row * a.k + t];
+                    oi_[t] = li == 0x7fffffff ? kSentinelIdx : a.index_base + li;
+                }
             }
         __syncwarp();
     }
@@ -310,20 +312,121 @@ size_t smem_bytes(int k, bool smem_lists) {
     return stages + (smem_lists ? lists : 0) + scratch;
 }
 
+// Merge of the blocks that span several CTAs: warp per query, the segment
+// slots first + b .. last + b of its block (sorted raw lists), first adopted,
+// the rest offered in 128-entry chunks with an early exit once a chunk's head
+// fails the running threshold.  Queries of single-segment blocks are skipped
+// (the exact kernel wrote them final).
+constexpr int MX_WARPS = 4;
+
+template <int M, bool SMEM_LISTS>
+__global__ void __launch_bounds__(MX_WARPS * 32) merge_exact_kernel(ExactArgs a, float* gk, int64_t* gi) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int k = a.k;
+    const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
+    const ExactSplit sp = exact_split(n_eff, a.ntiles, a.max_ctas);
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * MX_WARPS + warp; q < n_eff;
+         q += static_cast<int64_t>(gridDim.x) * MX_WARPS) {
+        const int64_t b = q / QT;
+        const int row = static_cast<int>(q - b * QT);
+        const int64_t first = sp.cta_of(b * a.ntiles), last = sp.cta_of((b + 1) * a.ntiles - 1);
+        if (first == last) continue;
+        float* lk;
+        int64_t* li;
+        if constexpr (SMEM_LISTS) {
+            lk = reinterpret_cast<float*>(smem_raw) + warp * k;
+            li = reinterpret_cast<int64_t*>(smem_raw + ((MX_WARPS * k * 4 + 15) / 16) * 16) + warp * k;
+        } else {
+            lk = gk + q * k;
+            li = gi + q * k;
+        }
+        WarpList<int64_t> L{lk, li, k};
+        auto part = [&](int64_t c) { return (static_cast<size_t>(c + b) * QT + row) * k; };
+        for (int t = lane; t < k; t += 32) {
+            lk[t] = a.part_key[part(first) + t];
+            li[t] = a.part_idx[part(first) + t];
+        }
+        __syncwarp();
+        for (int64_t c = first + 1; c <= last; ++c) {
+            const float* pk = a.part_key + part(c);
+            const int64_t* pi = a.part_idx + part(c);
+            for (int t0 = 0; t0 < k; t0 += 128) {
+                float ck[4];
+                int64_t ci[4];
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const int t = t0 + lane + 32 * s;
+                    ck[s] = t < k ? pk[t] : kInf;
+                    ci[s] = t < k ? pi[t] : kSentinelIdx;
+                }
+                float tk;
+                int64_t ti;
+                L.threshold(tk, ti);
+                const float hk = __shfl_sync(0xffffffffu, ck[0], 0);
+                const int64_t hi = __shfl_sync(0xffffffffu, ci[0], 0);
+                if (!pair_less(hk, hi, tk, ti)) break;  // sorted part: the rest fails too
+                L.offer<4>(ck, ci, lane);
+            }
+        }
+        __syncwarp();
+        if (!a.raw_keys) finalize_list(lk, li, k, M, lane);
+        const int64_t orow = a.qlist ? static_cast<int64_t>(a.qlist[q]) : q;
+        for (int t = lane; t < k; t += 32) {
+            a.out_key[orow * k + t] = lk[t];
+            a.out_idx[orow * k + t] = li[t];
+        }
+        __syncwarp();
+    }
+}
+
+constexpr int kMergeSmemMaxK = 2048;
+
 template <int M>
-void launch_exact_m(const ExactArgs& a, cudaStream_t stream) {
+void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
+    ExactArgs a = a_in;
     const bool smem_lists = a.glist_key == nullptr;
     const size_t smem = smem_bytes(a.k, smem_lists);
-    const dim3 grid(static_cast<unsigned>(a.ctas));
+    a.max_ctas = exact_max_ctas(a.k, smem_lists);
     const int kp = (a.k + 31) / 32;
     void (*kern)(ExactArgs) = !smem_lists ? exact_knn_kernel<M, 0>
-                              : kp == 1   ? exact_knn_kernel<M, 1>
+                              : kp == 1   ? (a.qlist ? exact_knn_kernel<M, 1, true> : exact_knn_kernel<M, 1>)
                               : kp == 2   ? exact_knn_kernel<M, 2>
                                           : exact_knn_kernel<M, 4>;
+    if (a.qlist && !(smem_lists && kp == 1)) throw CudaError("exact kernel: query lists need k <= 32");
     KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-    ProfileScope ps(stream, smem_lists ? "exact_knn_kernel" : "exact_knn_kernel_glist");
-    kern<<<grid, THREADS, smem, stream>>>(a);
+    {
+        ProfileScope ps(stream, smem_lists ? "exact_knn_kernel" : "exact_knn_kernel_glist");
+        kern<<<a.max_ctas, THREADS, smem, stream>>>(a);
+    }
+    KNN_LAUNCH_CHECK();
+    // merge the blocks spread over several CTAs (host-known counts: only if any)
+    if (!a.qcount) {
+        const ExactSplit sp = exact_split(a.n, a.ntiles, a.max_ctas);
+        const int64_t nqb = (a.n + QT - 1) / QT;
+        bool any = false;
+        for (int64_t b = 0; b < nqb && !any; ++b)
+            any = sp.cta_of(b * a.ntiles) != sp.cta_of((b + 1) * a.ntiles - 1);
+        if (!any) return;
+    }
+    const bool mx_smem = a.k <= kMergeSmemMaxK;
+    if (!mx_smem && !a.mglist_key) throw CudaError("merge_exact: k > 2048 needs list scratch");
+    const size_t mx_bytes = mx_smem ? ((MX_WARPS * static_cast<size_t>(a.k) * 4 + 15) / 16) * 16 +
+                                          MX_WARPS * static_cast<size_t>(a.k) * 8
+                                    : 0;
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((a.n + MX_WARPS - 1) / MX_WARPS, 16 * kSmCount)));
+    ProfileScope ps(stream, "merge_exact_kernel");
+    if (mx_smem) {
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(merge_exact_kernel<M, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(mx_bytes)));
+        merge_exact_kernel<M, true><<<grid, MX_WARPS * 32, mx_bytes, stream>>>(a, nullptr, nullptr);
+    } else {
+        merge_exact_kernel<M, false><<<grid, MX_WARPS * 32, 0, stream>>>(a, a.mglist_key, a.mglist_idx);
+    }
     KNN_LAUNCH_CHECK();
 }
 
@@ -334,24 +437,16 @@ size_t exact_smem_list_limit_k() {
     return 128;
 }
 
-void exact_plan(ExactArgs& a, bool smem_lists) {
+int exact_max_ctas(int k, bool smem_lists) {
     // resident CTAs: 2 per SM while the shared-memory footprint allows it
-    const size_t smem = smem_bytes(a.k, smem_lists);
-    const int per_sm = smem <= 113 * 1024 ? 2 : 1;  // 228 KB per SM, 1 KB reserved per CTA
-    const int64_t nqb = (a.n + QT - 1) / QT;
-    a.ntiles = static_cast<int>((a.m + RT - 1) / RT);
-    a.units = nqb * a.ntiles;
-    // every CTA keeps >= 8 tiles (1024 references) so lists amortise their fill
-    const int64_t by_work = std::max<int64_t>(1, a.units / 8);
-    a.ctas = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(kSmCount) * per_sm, by_work));
-    // parts: the most CTAs any query block is spread over
-    const int64_t W = a.units, G = a.ctas;
-    auto cta_of = [&](int64_t x) { return ((x + 1) * G + W - 1) / W - 1; };
-    int parts = 1;
-    for (int64_t b = 0; b < nqb; ++b)
-        parts = std::max<int>(parts, static_cast<int>(cta_of((b + 1) * a.ntiles - 1) -
-                                                      cta_of(b * a.ntiles) + 1));
-    a.parts = parts;
+    const size_t smem = smem_bytes(k, smem_lists);
+    return kSmCount * (smem <= 113 * 1024 ? 2 : 1);  // 228 KB per SM, 1 KB reserved per CTA
+}
+
+int exact_ntiles(int64_t m) { return static_cast<int>((m + RT - 1) / RT); }
+
+int64_t exact_slots(int64_t n, int ntiles, int max_ctas) {
+    return exact_split(n, ntiles, max_ctas).G + (n + QT - 1) / QT;
 }
 
 int exact_queries_per_cta() { return QT; }

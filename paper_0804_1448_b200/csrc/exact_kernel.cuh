@@ -7,24 +7,54 @@
 namespace knnb200 {
 
 struct ExactArgs {
-    const float* Q;          // n x d
+    const float* Q;          // query rows (row i of the search = Q row qlist ? qlist[i] : i)
     const float* R;          // m x d
-    int64_t n, m;
+    int64_t n, m;            // n: queries (the maximum when qcount is set)
     int d, k;
-    int64_t units;           // stream-K work units: query blocks x reference tiles
-    int ntiles;              // reference tiles per query block
-    int ctas;                // grid size (each CTA owns a contiguous unit range)
-    int parts;               // output slots per query (max CTAs sharing a query block)
+    int ntiles;              // reference tiles per query block (exact_plan)
+    const int* qlist;        // nullable: query i's row in Q and in the outputs
+    const int* qcount;       // nullable: device-side query count (<= n)
     int64_t index_base;      // added to every emitted index
-    float* out_key;          // [parts][n][k]
-    int64_t* out_idx;        // [parts][n][k]
-    int finalize;            // 1: out_key = finalized distance (parts == 1 only)
+    int raw_keys;            // 1: outputs keep raw keys (no finalize)
+    float* out_key;          // final outputs, n x k rows
+    int64_t* out_idx;
+    // Stream-K segments (CTA c, query block b) that share a block write their
+    // raw lists to slot c + b of [slots][128][k]; a block with one segment is
+    // emitted final by the exact kernel, the others by merge_exact.
+    float* part_key;
+    int64_t* part_idx;
     float* glist_key;        // global list scratch when k is too large for smem
     int32_t* glist_idx;
+    float* mglist_key;       // merge list scratch (n x k) when k > 2048
+    int64_t* mglist_idx;
+    int max_ctas;            // set by launch_exact (grid of the exact kernel)
 };
 
-// Work split of the exact kernel over the GPU: fills units/ntiles/ctas/parts.
-void exact_plan(ExactArgs& a, bool smem_lists);
+// Stream-K split of the exact path, a pure function of the query count so the
+// device can re-derive it from a device-side count: G CTAs (<= max_ctas, >= 8
+// tiles each) own contiguous ranges of the (query block, tile) units.
+struct ExactSplit {
+    int64_t units;
+    int64_t G;
+    __host__ __device__ int64_t start(int64_t c) const { return c * units / G; }
+    __host__ __device__ int64_t cta_of(int64_t x) const { return ((x + 1) * G + units - 1) / units - 1; }
+};
+__host__ __device__ inline ExactSplit exact_split(int64_t n, int ntiles, int max_ctas) {
+    const int64_t nqb = (n + 127) / 128;
+    ExactSplit s;
+    s.units = nqb * ntiles;
+    const int64_t by_work = s.units / 8 > 1 ? s.units / 8 : 1;
+    s.G = by_work < max_ctas ? by_work : max_ctas;
+    return s;
+}
+
+// Resident CTAs of the exact kernel (grid size) and reference tiles per block.
+int exact_max_ctas(int k, bool smem_lists);
+int exact_ntiles(int64_t m);
+// partial-list slots for up to n queries: G + query blocks
+int64_t exact_slots(int64_t n, int ntiles, int max_ctas);
+// exact kernel (grid = max CTAs; the CTAs past the split's G exit) followed by
+// merge_exact when some block spans several CTAs (always when qcount is set)
 void launch_exact(int metric, const ExactArgs& a, cudaStream_t stream);
 size_t exact_smem_list_limit_k();
 int exact_queries_per_cta();

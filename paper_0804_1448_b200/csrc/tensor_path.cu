@@ -1855,6 +1855,14 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     sz.take<float>(large ? static_cast<size_t>(n_pad) : 0);
     sz.take<float2>(static_cast<size_t>(parts) * TILE * CV);
     sz.take<int>(static_cast<size_t>(pairs));
+    // small k: the certification fallback runs on the device (exact kernel over
+    // the failed queries, count read on the device): its partial-list slots
+    const int fb_ctas = exact_max_ctas(k, true);
+    const size_t fb_part = large ? 0
+                                 : static_cast<size_t>(exact_slots(n, exact_ntiles(m), fb_ctas)) *
+                                       exact_queries_per_cta() * k;
+    sz.take<float>(fb_part);
+    sz.take<int64_t>(fb_part);
     ctx.arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -1871,6 +1879,8 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     float* t0 = cv.take<float>(large ? static_cast<size_t>(n_pad) : 0);
     float2* vlog = cv.take<float2>(static_cast<size_t>(parts) * TILE * CV);
     int* pair_slots = cv.take<int>(static_cast<size_t>(pairs));
+    float* fb_pk = cv.take<float>(fb_part);
+    int64_t* fb_pi = cv.take<int64_t>(fb_part);
     const unsigned* gmax = refs.gmax;
 
     // 1. per-search state and the query-side prep
@@ -2060,8 +2070,33 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     KNN_LAUNCH_CHECK();
 
     // 4. certification fallback (exact kernel on the failed queries), unless
-    //    the caller collects them across several searches
+    //    the caller collects them across several searches.  Small k: entirely
+    //    on the device -- no host round trip, the search stays asynchronous.
     if (sink) return;
+    if (!ctx.fb_dev) KNN_CUDA_CHECK(cudaMalloc(&ctx.fb_dev, sizeof(int)));
+    if (!large) {
+        ExactArgs ea{};
+        ea.Q = dQ;
+        ea.R = dR;
+        ea.n = n;
+        ea.m = m;
+        ea.d = d;
+        ea.k = k;
+        ea.ntiles = exact_ntiles(m);
+        ea.qlist = fb + 1;
+        ea.qcount = fb;
+        ea.index_base = index_base;
+        ea.raw_keys = raw_keys;
+        ea.out_key = d_out;
+        ea.out_idx = d_idx;
+        ea.part_key = fb_pk;
+        ea.part_idx = fb_pi;
+        launch_exact(kL2, ea, stream);
+        KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        ctx.fb_on_device = true;
+        return;
+    }
+    ctx.fb_on_device = false;
     int fails = 0;
     KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
     KNN_CUDA_CHECK(cudaStreamSynchronize(stream));

@@ -46,7 +46,7 @@ if __name__ == "__main__":
     else:
         n, m, d, k = (args + [38400, 38400, 96, 20][len(args):])[:4]
         reps = args[4] if len(args) > 4 else 5
-        for mode in (0, 2):
+        for mode in (0, 2, 3):
             env = dict(os.environ, KNN_B200_FILTER_MODE=str(mode), _FM_CHILD="1")
             subprocess.run([sys.executable, __file__, str(n), str(m), str(d), str(k),
                             str(reps if mode == 0 else 2)], env=env, check=False)
