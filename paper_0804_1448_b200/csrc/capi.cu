@@ -256,7 +256,8 @@ namespace {
 
 // queries per pipeline stage (multiple of 256): large enough that a chunk's
 // search runs near full efficiency (one chunk per ~128 query-tile pairs)
-constexpr int64_t kPipeChunk = 32768;
+constexpr int64_t kPipeChunk = 32768;     // largest query chunk of the pipelined host search
+constexpr int64_t kPipeMinChunk = 16384;  // smallest (below 2x this: one staged search)
 
 unsigned scan_grid(int64_t count) {
     return static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 1184));
@@ -332,30 +333,48 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), s));
-    KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * d, cudaMemcpyHostToDevice, s));
+    // every H2D goes through the copy stream in order (R, then the query
+    // chunks): the reference prep overlaps the first chunk's copy
+    KNN_CUDA_CHECK(cudaEventRecord(ctx.ev[0], s));
+    KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx.ev[0], 0));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(dR, r, sizeof(float) * m * d, cudaMemcpyHostToDevice, cs));
+    KNN_CUDA_CHECK(cudaEventRecord(ctx.ev[15], cs));
+    KNN_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.ev[15], 0));
     finite_scan_kernel<<<scan_grid(m * d), 256, 0, s>>>(dR, m * d, dbad + 1);
     KNN_LAUNCH_CHECK();
     TensorRefs refs;
     tensor_prep_refs(s, dR, m, d, ctx.refs.base(), refs);
-    // the copy stream may only start once the events of the previous call are done
-    KNN_CUDA_CHECK(cudaEventRecord(ctx.ev[0], s));
-    KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx.ev[0], 0));
-    const int64_t chunks = (n + kPipeChunk - 1) / kPipeChunk;
+    // chunks of <= 32 K queries, at least two (n >= 2 * kPipeMinChunk here),
+    // multiples of the 256-query tile pair
+    const int64_t chunks = std::max<int64_t>(2, (n + kPipeChunk - 1) / kPipeChunk);
+    const int64_t csz = ((n + chunks - 1) / chunks + 255) / 256 * 256;
     FallbackSink sink{fb, fb + 1, 0};
-    for (int64_t c = 0; c < chunks; ++c) {
-        const int64_t q0 = c * kPipeChunk, nq = std::min(kPipeChunk, n - q0);
-        cudaEvent_t in = ctx.ev[1 + 2 * (c % 7)], done = ctx.ev[2 + 2 * (c % 7)];
+    const int64_t nch = (n + csz - 1) / csz;
+    while (static_cast<int64_t>(ctx.pipe_ev.size()) < 2 * nch) {
+        cudaEvent_t e;
+        KNN_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx.pipe_ev.push_back(e);
+    }
+    // 1. every chunk's H2D, back to back on the copy stream (a chunk's D2H
+    //    queued between them would hold the next copy behind a search)
+    for (int64_t c = 0; c < nch; ++c) {
+        const int64_t q0 = c * csz, nq = std::min(csz, n - q0);
         KNN_CUDA_CHECK(cudaMemcpyAsync(dQ + q0 * d, q + q0 * d, sizeof(float) * nq * d,
                                        cudaMemcpyHostToDevice, cs));
-        KNN_CUDA_CHECK(cudaEventRecord(in, cs));
-        KNN_CUDA_CHECK(cudaStreamWaitEvent(s, in, 0));
+        KNN_CUDA_CHECK(cudaEventRecord(ctx.pipe_ev[2 * c], cs));
+    }
+    // 2. per chunk: validate + search as soon as its rows landed; its D2H
+    //    (copy stream, after all H2D) overlaps the next chunk's search
+    for (int64_t c = 0; c < nch; ++c) {
+        const int64_t q0 = c * csz, nq = std::min(csz, n - q0);
+        KNN_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.pipe_ev[2 * c], 0));
         finite_scan_kernel<<<scan_grid(nq * d), 256, 0, s>>>(dQ + q0 * d, nq * d, dbad, q0 * d);
         KNN_LAUNCH_CHECK();
         sink.offset = static_cast<int>(q0);
         tensor_search(ctx, s, refs, dQ + q0 * d, nq, k, raw_keys, 0, dO + q0 * k, dI + q0 * k,
                       &sink);
-        KNN_CUDA_CHECK(cudaEventRecord(done, s));
-        KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, done, 0));
+        KNN_CUDA_CHECK(cudaEventRecord(ctx.pipe_ev[2 * c + 1], s));
+        KNN_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx.pipe_ev[2 * c + 1], 0));
         KNN_CUDA_CHECK(cudaMemcpyAsync(out_dist + q0 * k, dO + q0 * k, sizeof(float) * nq * k,
                                        cudaMemcpyDeviceToHost, cs));
         KNN_CUDA_CHECK(cudaMemcpyAsync(out_idx + q0 * k, dI + q0 * k, sizeof(int64_t) * nq * k,
@@ -469,7 +488,7 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         if (plan_search(n, m, dq, k, kernel_metric, o.path).path == 2 && !host_values &&
-            n >= 2 * kPipeChunk)
+            n >= 2 * kPipeMinChunk)
             search_pipelined(ctx, q, n, r, m, dq, k, o.raw_keys, out_dist, out_idx);
         else
             search_staged(ctx, q, n, r, m, dq, dr, k, kernel_metric, o.path, o.raw_keys, host_values,

@@ -49,6 +49,7 @@ struct DeviceContext {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;   // host API: H2D / D2H overlapped with compute
     cudaEvent_t ev[16] = {};              // host API pipeline events
+    std::vector<cudaEvent_t> pipe_ev;     // per-chunk events of the pipelined host search
     DeviceArena arena;       // per-search scratch
     DeviceArena io;          // host-API staging of inputs / outputs
     DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
