@@ -10,6 +10,7 @@
 // knn_b200_last_error(); the C++ mirror rethrows them as std::invalid_argument.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -256,8 +257,15 @@ namespace {
 
 // queries per pipeline stage (multiple of 256): large enough that a chunk's
 // search runs near full efficiency (one chunk per ~128 query-tile pairs)
-constexpr int64_t kPipeChunk = 32768;     // largest query chunk of the pipelined host search
-constexpr int64_t kPipeMinChunk = 16384;  // smallest (below 2x this: one staged search)
+// largest query chunk of the pipelined host search (dev knob KNN_B200_PIPE_CHUNK);
+// below 2 x half of it, one staged search
+int64_t pipe_chunk() {
+    static const int64_t v = [] {
+        const char* e = getenv("KNN_B200_PIPE_CHUNK");
+        return e ? std::max<int64_t>(512, atoll(e)) : int64_t{32768};
+    }();
+    return v;
+}
 
 unsigned scan_grid(int64_t count) {
     return static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 1184));
@@ -344,9 +352,9 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     KNN_LAUNCH_CHECK();
     TensorRefs refs;
     tensor_prep_refs(s, dR, m, d, ctx.refs.base(), refs);
-    // chunks of <= 32 K queries, at least two (n >= 2 * kPipeMinChunk here),
+    // chunks of <= pipe_chunk() queries, at least two (n >= pipe_chunk() here),
     // multiples of the 256-query tile pair
-    const int64_t chunks = std::max<int64_t>(2, (n + kPipeChunk - 1) / kPipeChunk);
+    const int64_t chunks = std::max<int64_t>(2, (n + pipe_chunk() - 1) / pipe_chunk());
     const int64_t csz = ((n + chunks - 1) / chunks + 255) / 256 * 256;
     FallbackSink sink{fb, fb + 1, 0};
     const int64_t nch = (n + csz - 1) / csz;
@@ -488,7 +496,7 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         if (plan_search(n, m, dq, k, kernel_metric, o.path).path == 2 && !host_values &&
-            n >= 2 * kPipeMinChunk)
+            n >= pipe_chunk())
             search_pipelined(ctx, q, n, r, m, dq, k, o.raw_keys, out_dist, out_idx);
         else
             search_staged(ctx, q, n, r, m, dq, dr, k, kernel_metric, o.path, o.raw_keys, host_values,
