@@ -605,10 +605,12 @@ __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUten
     }
 }
 
-// warp 1, one elected thread: per unit two M=128 N=128 MMA chains (one per
-// query tile) into TMEM buffer [query tile][unit parity]
+// One elected thread per query tile g (warps 1 and 3): per unit an M=128
+// N=128 MMA chain into TMEM buffer [g][unit parity].  Two issuers, so a slow
+// epilogue group of one query tile never holds back the other tile's MMAs;
+// each commits to the shared stage / A-tile barriers (arrival count 2).
 __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int64_t ub, int64_t ue,
-                                         int W) {
+                                         int W, int g) {
     const uint32_t idesc = sm100::idesc_f16_f32(TILE, TILE);
     int stage = 0;
     uint32_t phase = 0, a_par = 0;
@@ -628,7 +630,7 @@ __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int
         sm100::mbar_wait(P.full + stage, phase);
         sm100::tc_fence_after();
         const uint32_t b0 = sm100::smem_u32(P.Bs + stage * P.KBB);
-        for (int g = 0; g < 2; ++g) {
+        {
             sm100::mbar_wait(P.tempty + 2 * g + b, tpar ^ 1u);
             sm100::tc_fence_after();
             const uint32_t a0 = sm100::smem_u32(P.As + g * P.KBB);
@@ -688,10 +690,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             sm100::mbar_init(full + s, 1);
-            sm100::mbar_init(empty + s, 1);
+            sm100::mbar_init(empty + s, 2);
         }
         sm100::mbar_init(a_full, 1);
-        sm100::mbar_init(a_empty, 1);
+        sm100::mbar_init(a_empty, 2);
         for (int b = 0; b < 4; ++b) {
             sm100::mbar_init(tfull + b, 1);
             sm100::mbar_init(tempty + b, 4);
@@ -710,7 +712,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0) {
         if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, 0);
     } else if (warp == 1) {
-        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0);
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0, 0);
+    } else if (warp == 3) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0, 1);
     } else if (warp >= 4) {
         // ------------------------------------------------- epilogue -------
         sm100::reg_alloc<EPI_REGS>();
@@ -947,10 +951,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
             sm100::mbar_init(full + s, 1);
-            sm100::mbar_init(empty + s, 1);
+            sm100::mbar_init(empty + s, 2);
         }
         sm100::mbar_init(a_full, 1);
-        sm100::mbar_init(a_empty, 1);
+        sm100::mbar_init(a_empty, 2);
         for (int b = 0; b < 4; ++b) {
             sm100::mbar_init(tfull + b, 1);
             sm100::mbar_init(tempty + b, 4);
@@ -968,7 +972,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0) {
         if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, a.W);
     } else if (warp == 1) {
-        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W);
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W, 0);
+    } else if (warp == 3) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W, 1);
     } else if (warp >= 4) {
         sm100::reg_alloc<EPI_REGS>();
         const int ew = warp - 4;
