@@ -1,0 +1,229 @@
+// knn_b200_cli -- the reference CLI's `search` subcommand on the B200 engine.
+//
+// Mirrors /root/reference/proj/tools/knn_cli.cpp (run_search, :66-96, and the
+// option table of main, :232-244) and the point/matrix CSV readers of
+// src/csv.cpp (read_rows :44-76, parse_double :24-31, read_points_csv :85-94,
+// read_matrix_csv :150-166): same options, same output
+//   query_index,rank,ref_index,distance
+// one row per (query, rank), written atomically through `<out>.tmp` + rename
+// (write_output, :42-56), and the same exit codes (main, :277-292): 0 success,
+// 2 malformed input file ("error: line N: ..."), 3 contract violation
+// (std::invalid_argument), 1 anything else, 2 for unknown options.
+//
+// Differences a caller can see: the search runs on the GPU in FP32 (distances
+// are printed as the shortest decimal of the FP32 value, so the reference's
+// CLI test fixture prints identically: 0.1 / 0.9 / 1.9), and `--method kdtree`
+// runs the same exact search (the kd-tree reports the same neighbours,
+// test_cli.cpp:70-75); --workers / --chunk-size / --leaf-size are accepted
+// and do not change results.
+#include <charconv>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <system_error>
+#include <vector>
+
+#include "knn_b200/bruteforce.hpp"
+
+namespace {
+
+struct CsvError : std::runtime_error {  // csv.hpp:16-25
+    CsvError(const std::string& message, std::size_t line)
+        : std::runtime_error("line " + std::to_string(line) + ": " + message) {}
+};
+
+struct UsageError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+std::string_view trim(std::string_view t) {
+    while (!t.empty() && (t.front() == ' ' || t.front() == '\t')) t.remove_prefix(1);
+    while (!t.empty() && (t.back() == ' ' || t.back() == '\t' || t.back() == '\r'))
+        t.remove_suffix(1);
+    return t;
+}
+
+double parse_double(std::string_view token, std::size_t line) {
+    token = trim(token);
+    double value = 0.0;
+    const auto [ptr, ec] = std::from_chars(token.data(), token.data() + token.size(), value);
+    if (ec != std::errc{} || ptr != token.data() + token.size())
+        throw CsvError("cannot parse '" + std::string(token) + "' as a number", line);
+    return value;
+}
+
+struct RawRow {
+    std::vector<std::string> fields;
+    std::size_t line;
+};
+
+// blank lines and '#' comments skipped; every row as wide as the first
+std::vector<RawRow> read_rows(const std::filesystem::path& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open '" + path.string() + "'");
+    std::vector<RawRow> rows;
+    std::string line;
+    std::size_t line_no = 0, width = 0;
+    while (std::getline(in, line)) {
+        ++line_no;
+        const std::string_view view = trim(line);
+        if (view.empty() || view.front() == '#') continue;
+        RawRow row{{}, line_no};
+        const std::string text(view);
+        std::size_t start = 0;
+        while (true) {
+            const std::size_t comma = text.find(',', start);
+            row.fields.push_back(text.substr(start, comma - start));
+            if (comma == std::string::npos) break;
+            start = comma + 1;
+        }
+        if (width == 0)
+            width = row.fields.size();
+        else if (row.fields.size() != width)
+            throw CsvError("expected " + std::to_string(width) + " fields, got " +
+                               std::to_string(row.fields.size()),
+                           line_no);
+        rows.push_back(std::move(row));
+    }
+    return rows;
+}
+
+knn_b200::PointSet read_points_csv(const std::filesystem::path& path) {
+    const std::vector<RawRow> rows = read_rows(path);
+    if (rows.empty()) throw CsvError("no data rows in " + path.string(), 0);
+    const std::size_t d = rows.front().fields.size();
+    std::vector<double> data;
+    data.reserve(rows.size() * d);
+    for (const RawRow& row : rows)
+        for (const std::string& f : row.fields) data.push_back(parse_double(f, row.line));
+    return knn_b200::PointSet(rows.size(), d, std::move(data));
+}
+
+std::vector<double> read_matrix_csv(const std::filesystem::path& path, std::size_t& dim) {
+    const std::vector<RawRow> rows = read_rows(path);
+    if (rows.empty()) throw CsvError("no data rows in " + path.string(), 0);
+    dim = rows.front().fields.size();
+    if (rows.size() != dim)
+        throw CsvError("matrix must be square, got " + std::to_string(rows.size()) + "x" +
+                           std::to_string(dim),
+                       rows.back().line);
+    std::vector<double> m;
+    m.reserve(dim * dim);
+    for (const RawRow& row : rows)
+        for (const std::string& f : row.fields) m.push_back(parse_double(f, row.line));
+    return m;
+}
+
+knn_b200::Metric parse_metric(const std::string& name) {
+    if (name == "euclidean") return knn_b200::Metric::euclidean();
+    if (name == "manhattan") return knn_b200::Metric::manhattan();
+    if (name == "chebyshev") return knn_b200::Metric::chebyshev();
+    if (name.rfind("mahalanobis:", 0) == 0) {
+        std::size_t dim = 0;
+        std::vector<double> m = read_matrix_csv(name.substr(std::string("mahalanobis:").size()), dim);
+        return knn_b200::Metric::mahalanobis(dim, std::move(m));
+    }
+    throw UsageError("--metric: expected euclidean, manhattan, chebyshev or mahalanobis:PATH");
+}
+
+void write_output(const std::string& path, const std::string& content) {
+    if (path.empty()) {
+        std::cout << content;
+        return;
+    }
+    const std::filesystem::path target(path);
+    std::filesystem::path temp = target;
+    temp += ".tmp";
+    {
+        std::ofstream out(temp, std::ios::trunc);
+        if (!out) throw std::runtime_error("cannot open '" + temp.string() + "' for writing");
+        out << content;
+    }
+    std::filesystem::rename(temp, target);
+}
+
+std::string format_distance(double d) {  // the FP32 value's shortest decimal
+    char buf[32];
+    const auto [ptr, ec] = std::to_chars(buf, buf + sizeof(buf), static_cast<float>(d));
+    return std::string(buf, ptr);
+}
+
+template <typename T>
+T parse_number(const std::string& opt, const std::string& v) {
+    T out{};
+    const auto [ptr, ec] = std::from_chars(v.data(), v.data() + v.size(), out);
+    if (ec != std::errc{} || ptr != v.data() + v.size())
+        throw UsageError(opt + ": '" + v + "' is not a valid number");
+    return out;
+}
+
+int run_search(int argc, char** argv) {
+    std::string ref_path, query_path, out_path, metric = "euclidean", method = "bf";
+    std::size_t k = 0, chunk_size = 1024;
+    bool have_k = false;
+    for (int i = 2; i < argc; ++i) {
+        const std::string opt = argv[i];
+        if (i + 1 >= argc) throw UsageError(opt + ": missing value");
+        const std::string val = argv[++i];
+        if (opt == "--ref") ref_path = val;
+        else if (opt == "--query") query_path = val;
+        else if (opt == "--out") out_path = val;
+        else if (opt == "--metric") metric = val;
+        else if (opt == "--method") method = val;
+        else if (opt == "--k") k = parse_number<std::size_t>(opt, val), have_k = true;
+        else if (opt == "--chunk-size") chunk_size = parse_number<std::size_t>(opt, val);
+        else if (opt == "--workers") parse_number<unsigned>(opt, val);
+        else if (opt == "--leaf-size") parse_number<std::size_t>(opt, val);
+        else throw UsageError("The following argument was not expected: " + opt);
+    }
+    if (ref_path.empty()) throw UsageError("--ref is required");
+    if (query_path.empty()) throw UsageError("--query is required");
+    if (!have_k) throw UsageError("--k is required");
+    if (method != "bf" && method != "kdtree") throw UsageError("--method: expected bf or kdtree");
+
+    const knn_b200::PointSet refs = read_points_csv(ref_path);
+    const knn_b200::PointSet queries = read_points_csv(query_path);
+    const knn_b200::Metric m = parse_metric(metric);
+    knn_b200::BfConfig config;
+    config.chunk_size = chunk_size;
+    const knn_b200::NeighborTable table = knn_b200::bf_knn(queries, refs, k, m, config);
+
+    std::ostringstream out;
+    out << "query_index,rank,ref_index,distance\n";
+    for (std::size_t i = 0; i < table.query_count(); ++i) {
+        const auto row = table.row(i);
+        for (std::size_t r = 0; r < row.size(); ++r)
+            out << i << ',' << r << ',' << row[r].index << ',' << format_distance(row[r].distance)
+                << '\n';
+    }
+    write_output(out_path, out.str());
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        if (argc < 2 || std::string(argv[1]) != "search")
+            throw UsageError("usage: knn_b200_cli search --ref R.csv --query Q.csv --k K "
+                             "[--metric M] [--method bf|kdtree] [--out OUT.csv]");
+        return run_search(argc, argv);
+    } catch (const UsageError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return 2;
+    } catch (const CsvError& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return 2;
+    } catch (const std::invalid_argument& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return 3;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return 1;
+    }
+}
