@@ -417,8 +417,7 @@ __device__ __forceinline__ void push_group_off(float gm, float tf, uint32_t& sgp
         "@p st.shared.f32 [%0], %2;\n\t"
         "mad.wide.s32 a, %1, 32, %5;\n\t"
         "mad.wide.s32 b, %1, 8, %6;\n\t"
-        "@q st.global.v4.f32 [a], {%8, %9, %10, %11};\n\t"
-        "@q st.global.v4.f32 [a+16], {%12, %13, %14, %15};\n\t"
+        "@q st.global.v8.f32 [a], {%8, %9, %10, %11, %12, %13, %14, %15};\n\t"
         "@q st.global.v2.b32 [b], {%2, %7};\n\t"
         "@p add.s32 %1, %1, 1;\n\t"
         "@p add.s32 %0, %0, %16;\n\t}"
@@ -1574,10 +1573,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
             for (int e = 0; e < 8; ++e) w[e] = kInf;
             if (j < ng) {
                 const int slot = gl[j];
-                const float4 u = a.f.log_v[2 * static_cast<int64_t>(slot)],
-                             v = a.f.log_v[2 * static_cast<int64_t>(slot) + 1];
-                w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
-                w[4] = v.x; w[5] = v.y; w[6] = v.z; w[7] = v.w;
+                ldg8(reinterpret_cast<const float*>(a.f.log_v + 2 * static_cast<int64_t>(slot)), w);
                 c0 = a.f.log_h[slot].y;
             }
             __syncwarp();
