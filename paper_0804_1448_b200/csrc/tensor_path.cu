@@ -756,7 +756,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
             if (kStats && a.stats) ++st_rounds;                                                            \
             const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
-            if (g_ <= Tf) L.insert(g_);                                                          \
+            /* a minimum at or above the list's last entry changes nothing */                  \
+            if (__any_sync(0xffffffffu, g_ <= Tf && g_ < L.key[KR - 1])) L.insert(g_);           \
         }                                                                                        \
         sgp = sg0;                                                                               \
         if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
