@@ -1316,7 +1316,10 @@ struct LargeArgs {
     int sort_variant;        // dev: 1 = all-shared-memory bitonic network
 };
 
-__global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
+// NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
+// capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
+template <int NT>
+__global__ void __launch_bounds__(NT) select_large_kernel(LargeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
     int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
@@ -1369,7 +1372,7 @@ __global__ void __launch_bounds__(LK_THREADS) select_large_kernel(LargeArgs a) {
             // compact the candidates (A <= tau) to the front, any order
             if (threadIdx.x == 0) s_cnt = 0;
             __syncthreads();
-            int mine[16];  // total <= NC <= 16 * LK_THREADS: a thread owns <= 16 entries
+            int mine[16];  // total <= NC <= 16 * NT: a thread owns <= 16 entries
             int nm = 0;
             for (int e = threadIdx.x; e < total; e += blockDim.x)
                 if (sk[e] <= tau) mine[nm++] = si[e];
@@ -2013,12 +2016,15 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         la.fb_list = sink ? sink->list : fb + 1;
         la.fb_offset = sink ? sink->offset : 0;
         const size_t sel_smem = static_cast<size_t>(NC) * 8;
-        KNN_CUDA_CHECK(cudaFuncSetAttribute(select_large_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const int nt = NC <= 16 * 64 ? 64 : NC <= 16 * 128 ? 128 : NC <= 16 * 256 ? 256 : LK_THREADS;
+        auto sel = nt == 64    ? select_large_kernel<64>
+                   : nt == 128 ? select_large_kernel<128>
+                   : nt == 256 ? select_large_kernel<256> : select_large_kernel<LK_THREADS>;
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(sel_smem)));
         {
             ProfileScope ps(stream, "select_large_kernel");
-            select_large_kernel<<<static_cast<unsigned>(n), LK_THREADS, sel_smem, stream>>>(la);
+            sel<<<static_cast<unsigned>(n), nt, sel_smem, stream>>>(la);
         }
         KNN_LAUNCH_CHECK();
     } else {
