@@ -322,6 +322,52 @@ def test_tensor_path_is_used_and_certified(knn, oracle):
 
 
 @pytest.mark.gpu
+def test_device_fallback_is_asynchronous_on_a_stream(knn, oracle):
+    """Index search on a caller stream: the certification fallback (exact
+    kernel over a device-side query list) runs without a host round trip, so
+    the call returns before the work is done; after a stream sync the table is
+    the exact one.  Mixed batch: uniform queries certify, queries sitting on a
+    heavily duplicated reference overflow their logs and fall back."""
+    import torch
+    d, k = 16, 20
+    base = oracle.uniform_f32(2000, d, 41)
+    dup = np.repeat(oracle.uniform_f32(1, d, 42), 30000, axis=0)
+    R = np.concatenate([base, dup]).astype(np.float32)
+    Q = np.concatenate([oracle.uniform_f32(300, d, 43), dup[:40] + 1e-4]).astype(np.float32)
+    n, m = Q.shape[0], R.shape[0]
+    Qd, Rd = torch.from_numpy(Q).cuda(), torch.from_numpy(R).cuda()
+    od = torch.empty((n, k), device="cuda")
+    oi = torch.empty((n, k), dtype=torch.int64, device="cuda")
+    ix = knn.Index(device_ptr=Rd.data_ptr(), m=m, d=d)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ix.search_device(Qd.data_ptr(), n, k, od.data_ptr(), oi.data_ptr(),
+                         stream=s.cuda_stream)
+    s.synchronize()
+    assert knn.last_fallback_count() > 0
+    te = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (oi.cpu().numpy() == te.index).all()
+    assert (od.cpu().numpy() == te.distance).all()
+    ix.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [33, 64, 129, 500])
+def test_large_k_block_sizes(knn, oracle, k):
+    """The large-k selection picks 64 / 128 / 256 / 512-thread blocks from the
+    candidate capacity; every size must give the exact table."""
+    m, d = 12000, 24
+    R = oracle.uniform_f32(m, d, 600 + k)
+    Q = oracle.uniform_f32(128, d, 700 + k)
+    ri, rd = oracle.knn(Q, R, k)
+    t = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+    assert rep.ok, f"k={k}: {rep}"
+    te = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (t.index == te.index).all() and (t.distance == te.distance).all()
+
+
+@pytest.mark.gpu
 def test_non_finite_detected_on_device(knn, oracle):
     """The host API validates coordinates on the device copy (point_set.hpp:27-31
     text, first offending coordinate in row-major order)."""
