@@ -65,7 +65,7 @@ __device__ __forceinline__ float key_step(float acc, float q, float r) {
     } else if constexpr (M == kL1) {
         return __fadd_rn(acc, fabsf(t));
     } else {
-        return fabsf(t) > acc ? fabsf(t) : acc;
+        return fmaxf(acc, fabsf(t));  // = (|t| > acc ? |t| : acc) on finite keys
     }
 }
 

@@ -60,16 +60,19 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const float* src, bool v
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Two key_step<M> updates at once: acc.{x,y} = key_step(acc.{x,y}, q, r.{x,y}).
-// For L2 this is one packed FADD2 (q broadcast, r negated by an operand
-// modifier: q + (-r) == q - r exactly) and one packed FFMA2.
+// Two key_step<M> updates at once: acc.{x,y} = key_step(acc.{x,y}, q, r.{x,y}),
+// bitwise: one packed FADD2 for the differences (q broadcast, r negated by an
+// operand modifier: q + (-r) == q - r exactly), then FFMA2 (L2), FADD2 with
+// |t| (L1) or per-lane maxima (L-inf).
 template <int M>
 __device__ __forceinline__ float2 key_step2(float2 acc, float q, float2 r) {
+    const float2 t = __fadd2_rn(make_float2(q, q), make_float2(-r.x, -r.y));
     if constexpr (M == kL2) {
-        const float2 t = __fadd2_rn(make_float2(q, q), make_float2(-r.x, -r.y));
         return __ffma2_rn(t, t, acc);
-    } else {
-        return make_float2(key_step<M>(acc.x, q, r.x), key_step<M>(acc.y, q, r.y));
+    } else if constexpr (M == kL1) {  // packed add with the |t| operand modifier
+        return __fadd2_rn(acc, make_float2(fabsf(t.x), fabsf(t.y)));
+    } else {  // consecutive maxima fuse into FMNMX3 (max is exact, order-free)
+        return make_float2(fmaxf(acc.x, fabsf(t.x)), fmaxf(acc.y, fabsf(t.y)));
     }
 }
 
