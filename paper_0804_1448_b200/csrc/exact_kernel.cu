@@ -76,11 +76,14 @@ __device__ __forceinline__ float2 key_step2(float2 acc, float q, float2 r) {
     }
 }
 
-// KP: list entries per lane of the register-resident list (k <= 32 KP, lists in
-// shared memory), or 0 for lists in global memory (k > 128, WarpList).
+// KP > 0: lists in shared memory, offered in register bursts of KP entries per
+// lane (k <= 32 KP); KP < 0: lists in global memory, register bursts of -KP
+// (128 < k <= 256); 0: lists in global memory, WarpList (k > 256; larger
+// register bursts spill).
 template <int M, int KP, bool INDIRECT = false>
 __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
-    constexpr bool SMEM_LISTS = KP > 0;
+    constexpr bool SMEM_LISTS = KP > 0;  // KP < 0: global lists, register bursts of -KP
+    constexpr int RP = KP > 0 ? KP : -KP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* stages = reinterpret_cast<float*>(smem_raw);      // [NSTAGE][STAGE]
     float* Lk = stages + NSTAGE * STAGE;                       // [QT][k] (smem lists)
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
                     for (int h = 0; h < 2; ++h) {
                         if (((vote >> (16 * h)) & 0xffffu) == 0u) continue;
                         const int row = 2 * warp + h + 16 * i;
-                        if constexpr (KP > 0) {
+                        if constexpr (RP > 0) {
                             float ck[4];
                             int32_t ci[4];
 #pragma unroll
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
                                 ck[p] = ok ? sc[h * RT + col] : kInf;
                                 ci[p] = ok ? static_cast<int32_t>(t0 + col) : 0x7fffffff;
                             }
-                            WarpRegList<KP> L;
+                            WarpRegList<RP> L;
                             L.load(Lk + row * a.k, Li + row * a.k, a.k, lane);
                             if (L.offer<4>(ck, ci, a.k, lane)) L.store(Lk + row * a.k, Li + row * a.k, a.k, lane);
                         } else {
@@ -393,7 +396,7 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
     const size_t smem = smem_bytes(a.k, smem_lists);
     a.max_ctas = exact_max_ctas(a.k, smem_lists);
     const int kp = (a.k + 31) / 32;
-    void (*kern)(ExactArgs) = !smem_lists ? exact_knn_kernel<M, 0>
+    void (*kern)(ExactArgs) = !smem_lists ? (a.k <= 256 ? exact_knn_kernel<M, -8> : exact_knn_kernel<M, 0>)
                               : kp == 1   ? (a.qlist ? exact_knn_kernel<M, 1, true> : exact_knn_kernel<M, 1>)
                               : kp == 2   ? exact_knn_kernel<M, 2>
                                           : exact_knn_kernel<M, 4>;

@@ -1,7 +1,7 @@
 # dev: exact SIMT path timings (both register budgets) + GPU parity suite
 set -x
 for minb in 2; do
-for a in "38400 96 20 0" "38400 96 20 1" "38400 96 20 2" "38400 96 50 0" "38400 96 100 0" "38400 96 150 0" "38400 32 20 0" "38400 128 20 0" "38400 96 1 0"; do
+for a in "38400 96 300 0" "38400 96 512 0" "38400 96 1024 0"; do
   KNN_B200_EXACT_MINB=$minb timeout 120 python tools/prof_exact.py $a >> gpurun_out/exact.txt 2>&1
 done
 echo "---" >> gpurun_out/exact.txt
