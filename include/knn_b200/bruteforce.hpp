@@ -9,6 +9,7 @@
 //   knn::BfConfig        bruteforce.hpp:12-20    knn_b200::BfConfig (+ engine path)
 //   knn::SearchStats     bruteforce.hpp:22-25    knn_b200::SearchStats
 //   knn::bf_knn          bruteforce.hpp:31-33    knn_b200::bf_knn
+//   knn::bf_cost_model   bruteforce.hpp:35-43    knn_b200::bf_cost_model
 //
 // Header-only: every search goes through the C ABI (knn_b200.h) of
 // libknn_b200.so.  Coordinates are narrowed to FP32 at the boundary (the
@@ -191,6 +192,23 @@ inline NeighborTable bf_knn(const PointSet& queries, const PointSet& references,
     }
     if (stats) stats->distance_evals = evals;  // bruteforce.cpp:98
     return table;
+}
+
+// bruteforce.hpp:35-43, bruteforce.cpp:102-112: the paper's closed-form
+// operation counts of the exhaustive search.
+struct BfCostModel {
+    std::uint64_t additions;        // 2*n*m*d
+    std::uint64_t multiplications;  // n*m*d
+    double comparisons;             // n*m*log2(m)
+};
+
+inline BfCostModel bf_cost_model(std::size_t n, std::size_t m, std::size_t d, std::size_t k) {
+    if (n == 0 || m == 0 || d == 0 || k == 0)
+        throw std::invalid_argument("bf_cost_model: all inputs must be >= 1");
+    const std::uint64_t nmd = static_cast<std::uint64_t>(n) * m * d;
+    return BfCostModel{2 * nmd, nmd,
+                       static_cast<double>(n) * static_cast<double>(m) *
+                           std::log2(static_cast<double>(m))};
 }
 
 }  // namespace knn_b200

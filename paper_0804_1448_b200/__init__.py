@@ -13,6 +13,7 @@ raise ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 from typing import Optional
@@ -279,6 +280,22 @@ def bf_knn(queries, references, k: int, metric: Metric = None, config: BfConfig 
     if stats is not None:
         stats.distance_evals = int(evals.value)
     return NeighborTable(out_i, out_d)
+
+
+@dataclass
+class BfCostModel:
+    """bruteforce.hpp:35-43: the paper's closed-form operation counts."""
+    additions: int
+    multiplications: int
+    comparisons: float
+
+
+def bf_cost_model(n: int, m: int, d: int, k: int) -> BfCostModel:
+    """bruteforce.cpp:102-112: adds 2nmd, muls nmd, comparisons n m log2 m."""
+    if n <= 0 or m <= 0 or d <= 0 or k <= 0:
+        raise ValueError("bf_cost_model: all inputs must be >= 1")
+    nmd = n * m * d
+    return BfCostModel(2 * nmd, nmd, float(n) * float(m) * math.log2(float(m)))
 
 
 def search_device(q_ptr: int, n: int, r_ptr: int, m: int, d: int, k: int, out_dist_ptr: int,

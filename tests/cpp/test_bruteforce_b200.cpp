@@ -128,6 +128,14 @@ static void contract_errors() {
             (void)knn_b200::bf_knn(query, refs, 1, Metric::mahalanobis(3, {1, 0, 0, 0, 1, 0, 0, 0, 1}));
         },
         "Mahalanobis matrix is 3x3 but points have dimension 2");
+    // bf_cost_model (test_bruteforce.cpp cost cases; bruteforce.cpp:102-112)
+    {
+        const knn_b200::BfCostModel c = knn_b200::bf_cost_model(10, 100, 8, 5);
+        CHECK(c.additions == 16000u);
+        CHECK(c.multiplications == 8000u);
+        CHECK(std::abs(c.comparisons - 1000.0 * std::log2(100.0)) < 1e-9);
+        check_throws([&] { (void)knn_b200::bf_cost_model(0, 1, 1, 1); }, "all inputs must be >= 1");
+    }
 }
 
 static void gpu_cases() {

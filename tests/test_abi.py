@@ -94,3 +94,18 @@ def test_mahalanobis_validation(knn):
 def test_merge_argument_validation(knn):
     with pytest.raises(ValueError, match="parts, n and k must be >= 1"):
         knn.merge_device(0, 0, 0, 1, 1, 0, 0)
+
+
+def test_bf_cost_model_closed_forms():
+    """test_bruteforce.cpp:169-181: the paper's operation counts."""
+    import math
+    import paper_0804_1448_b200 as knn
+    unit = knn.bf_cost_model(1, 1, 1, 1)
+    assert (unit.additions, unit.multiplications, unit.comparisons) == (2, 1, 0.0)
+    c = knn.bf_cost_model(10, 100, 8, 5)
+    assert c.multiplications == 8000 and c.additions == 16000
+    assert abs(c.comparisons - 1000 * math.log2(100)) < 1e-9
+    d = knn.bf_cost_model(10, 100, 16, 5)
+    assert d.additions == 2 * c.additions and d.comparisons == c.comparisons
+    with pytest.raises(ValueError, match="all inputs must be >= 1"):
+        knn.bf_cost_model(0, 1, 1, 1)
