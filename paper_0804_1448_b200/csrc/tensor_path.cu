@@ -650,13 +650,15 @@ __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int
 }
 
 // Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
-// resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA,
-// one thread of warp 1 issues two M=128 N=128 MMA chains per reference tile
-// (one per query tile) into TMEM buffer (query tile g, unit parity b), and
-// epilogue set (g, b) -- 4 warps, one per TMEM lane quarter -- owns exactly
-// that buffer: thread = query row, all 128 columns of every other reference
-// tile.  16 epilogue warps (4 per SM sub-partition) hide the TMEM-load and
-// selection latencies; each query keeps one bound list per (CTA, parity).
+// resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA;
+// one thread of warp 1 (query tile 0) and one of warp 3 (query tile 1) issue
+// the M=128 N=128 MMA chain of their tile into TMEM buffer (g, unit parity);
+// warp 2 owns the TMEM allocation.  Epilogue set g -- 4 warps, one per TMEM
+// lane quarter -- reads both parity buffers of its tile in turn: thread =
+// query row, 128 columns per unit in four 32-column chunks (one TMEM load in
+// flight ahead of the scan).  Each query keeps one bound list per CTA part;
+// pushed groups go to the global group log, their minima to a shared-memory
+// buffer that the drain inserts into the list once per tile.
 template <int KR>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
@@ -1198,36 +1200,9 @@ __device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) 
     __syncthreads();
 }
 
-// All-shared-memory network (one barrier per stage), kept for comparison.
-__device__ void bitonic_sort_kv_smem(float* key, int* idx, int N) {
-    for (int size = 2; size <= N; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            __syncthreads();
-            for (int i = threadIdx.x; i < (N >> 1); i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const float ka = key[lo], kb = key[hi];
-                const int ia = idx[lo], ib = idx[hi];
-                if (pair_less(kb, ib, ka, ia) == up) {
-                    key[lo] = kb;
-                    key[hi] = ka;
-                    idx[lo] = ib;
-                    idx[hi] = ia;
-                }
-            }
-        }
-    }
-    __syncthreads();
-}
-
 // N (power of two, 32 <= N <= 16 * blockDim.x) pairs by the whole block:
 // one element per thread up to N = blockDim.x, then N / blockDim.x.
-__device__ void bitonic_sort_kv(float* key, int* idx, int N, int variant) {
-    if (variant == 1) {
-        bitonic_sort_kv_smem(key, idx, N);
-        return;
-    }
+__device__ void bitonic_sort_kv(float* key, int* idx, int N) {
     const int bd = static_cast<int>(blockDim.x);
     if (N <= bd) {
         bitonic_sort_kv_regs<1>(key, idx, N, N);
@@ -1313,7 +1288,6 @@ struct LargeArgs {
     int* fb_count;
     int* fb_list;
     int fb_offset;
-    int sort_variant;        // dev: 1 = all-shared-memory bitonic network
 };
 
 // NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
@@ -1403,7 +1377,7 @@ __global__ void __launch_bounds__(NT) select_large_kernel(LargeArgs a) {
         sk[e] = kInf;
         si[e] = 0x7fffffff;
     }
-    bitonic_sort_kv(sk, si, N2, a.sort_variant);
+    bitonic_sort_kv(sk, si, N2);
     // finalize: sqrt, then equal reported distances in ascending index order
     if (!a.raw_keys) {
         for (int t = threadIdx.x; t < k; t += blockDim.x) sk[t] = __fsqrt_rn(sk[t]);
@@ -1998,11 +1972,6 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         la.d = d;
         la.k = k;
         la.S_max = S_max;
-        static const int sort_variant = [] {
-            const char* e = getenv("KNN_B200_SORT");
-            return e ? atoi(e) : 0;
-        }();
-        la.sort_variant = sort_variant;
         int NC = 1;
         while (NC < 2 * margin * k) NC <<= 1;
         NC = std::min(NC, 16 * LK_THREADS);
