@@ -1,0 +1,497 @@
+// tensor_filter.cu -- the persistent tcgen05 filter kernels: the running-bound
+// filter of the small-k path (bound lists + group log) and the fixed-threshold
+// filter of the large-k path (seed tiles + value log).  DESIGN.md sec. 3.2-3.3.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "profile.cuh"
+#include "sm100.cuh"
+#include "tensor_internal.cuh"
+
+namespace knnb200 {
+namespace tp {
+
+namespace {
+
+// Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
+// resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA;
+// one thread of warp 1 (query tile 0) and one of warp 3 (query tile 1) issue
+// the M=128 N=128 MMA chain of their tile into TMEM buffer (g, unit parity);
+// warp 2 owns the TMEM allocation.  Epilogue set g -- 4 warps, one per TMEM
+// lane quarter -- reads both parity buffers of its tile in turn: thread =
+// query row, 128 columns per unit in four 32-column chunks (one TMEM load in
+// flight ahead of the scan).  Each query keeps one bound list per CTA part;
+// pushed groups go to the global group log, their minima to a shared-memory
+// buffer that the drain inserts into the list once per tile.
+template <int KR>
+__global__ void __launch_bounds__(THREADS, 1)
+    filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                  FilterArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-B aligned start, derived by offset so the compiler keeps the shared
+    // address space (LDS/STS instead of generic accesses)
+    unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
+    unsigned char* As = base;                // 2 query tiles
+    unsigned char* Bs = base + 2 * KBB;      // stages x reference tile
+    float* GB = reinterpret_cast<float*>(Bs + a.stages * KBB);        // [CAP][512] group minima
+    uint64_t* sT = reinterpret_cast<uint64_t*>(GB + CAP * EPI_THREADS);  // [2][128] tagged bounds
+    uint64_t* sP = sT + 2 * TILE;                                       // [2][2][128] tagged kp-th
+    uint64_t* bars = sP + 4 * TILE;
+    uint64_t* full = bars;
+    uint64_t* empty = bars + a.stages;
+    uint64_t* a_full = bars + 2 * a.stages;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* tfull = a_full + 2;  // [query tile][parity]
+    uint64_t* tempty = tfull + 4;  // [query tile][parity]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int64_t u_begin = unit_start(a.U, a.G, cta);
+    const int64_t u_end = unit_start(a.U, a.G, cta + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            sm100::mbar_init(full + s, 1);
+            sm100::mbar_init(empty + s, 2);
+        }
+        sm100::mbar_init(a_full, 1);
+        sm100::mbar_init(a_empty, 2);
+        for (int b = 0; b < 4; ++b) {
+            sm100::mbar_init(tfull + b, 1);
+            sm100::mbar_init(tempty + b, 4);
+        }
+        sm100::fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < 6 * TILE; i += blockDim.x) sT[i] = ~0ull;  // no tag matches
+    if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
+    const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
+    if (warp == 0) {
+        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, 0);
+    } else if (warp == 1) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0, 0);
+    } else if (warp == 3) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0, 1);
+    } else if (warp >= 4) {
+        // ------------------------------------------------- epilogue -------
+        sm100::reg_alloc<EPI_REGS>();
+        const int ew = warp - 4;          // 0..7
+        const int grp = ew >> 2;          // query tile of the pair
+        const int quarter = warp & 3;     // TMEM lane quarter
+        const int et = ew * 32 + lane;    // buffer column (0..255)
+        const int row = quarter * 32 + lane;
+        const int k = a.k;
+        const uint32_t sg0 = sm100::smem_u32(GB) + static_cast<uint32_t>(et) * 4;
+
+        RegList<KR> L;
+        L.reset();
+        int cur_p = -1;
+        uint32_t sgp = sg0;  // next buffer slot: (sgp - sg0) / (4 EPI_THREADS) minima buffered
+        float T = kInf;    // own bound: thresh(k-th smallest group minimum of this list)
+        float Tf = kInf;   // filter bound: min over every valid bound for this query
+        unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
+        Consts qc{};
+        int64_t q = 0;
+        int64_t part = 0;
+        const float4* lvb = nullptr;  // this (query, part)'s group log
+        const int2* lhb = nullptr;
+        int ln = 0;            // groups logged so far (may exceed CG: overflow)
+        unsigned long long st_drains = 0, st_rounds = 0;
+        long long st_cyc_drain = 0, st_cyc_wait = 0;
+        const long long st_cyc0 = kStats ? clock64() : 0;
+
+        // Drain: one buffered group minimum per lane per round into the bound
+        // list, then refresh the bound from (1) this list, (2) the other
+        // parity's list of the same query (smem, tagged by pair), (3) the union
+        // of both lists' ceil(k/2)-th values, (4) other CTAs' lists (global
+        // atomicMin, read one drain late so the load latency hides).
+#define KNN_DRAIN()                                                                              \
+    do {                                                                                         \
+        const long long c0_ = (kStats && a.stats) ? clock64() : 0;                                           \
+        if (kStats && a.stats) ++st_drains;                                                                \
+        const int nb = static_cast<int>((sgp - sg0) / (EPI_THREADS * 4));                       \
+        const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
+        _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
+            if (kStats && a.stats) ++st_rounds;                                                            \
+            const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
+            /* a minimum at or above the list's last entry changes nothing */                  \
+            if (__any_sync(0xffffffffu, g_ <= Tf && g_ < L.key[KR - 1])) L.insert(g_);           \
+        }                                                                                        \
+        sgp = sg0;                                                                               \
+        if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
+        float tf_ = fminf(T, dec_or_inf(tg_pref));                                               \
+        if (T < kInf) atomicMin(a.tglob + q, enc(T));                                            \
+        tg_pref = __ldcg(a.tglob + q);                                                           \
+        Tf = tf_;                                                                                \
+        if (kStats && a.stats) st_cyc_drain += clock64() - c0_;                                            \
+    } while (0)
+
+#define KNN_FLUSH()                                                                              \
+    do {                                                                                         \
+        float* pa_ = a.part_A + part * a.Kq * TILE;                                              \
+        _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_)                                        \
+            if (e_ < L.cnt) pa_[e_ * TILE + row] = L.key[e_];                                    \
+        a.part_cnt[part * TILE + row] = L.cnt;                                                   \
+        a.log_n[part * TILE + row] = ln;                                                         \
+    } while (0)
+
+        // One 32-column chunk, branch-free: the minimum of each 8-column group
+        // (FMNMX3); every group whose minimum is under the lane's bound is
+        // pushed (predicated stores): its minimum to the smem buffer, its 8
+        // values to the global log.  With 32 queries per warp some lane hits
+        // in most chunks, so a hit must not cost a divergent branch.
+#define KNN_SCAN_CHUNK(vv, colb)                                                                 \
+    do {                                                                                         \
+        float gm_[4];                                                                            \
+        bool any_ = false;                                                                       \
+        _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                       \
+            const float* w_ = vv + 8 * i_;                                                       \
+            gm_[i_] = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]), w_[6]),   \
+                            w_[7]);                                                              \
+            any_ |= gm_[i_] <= Tf;                                                               \
+        }                                                                                        \
+        if (a.mode != 3 && __any_sync(0xffffffffu, any_)) { /* some lane pushes: most chunks */ \
+            _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_)                                     \
+                push_group_off<EPI_THREADS * 4>(gm_[i_], Tf, sgp, ln, a.CG, lvb, lhb, vv + 8 * i_, \
+                                                (colb) + 8 * i_);                                \
+        }                                                                                        \
+    } while (0)
+
+        int p = static_cast<int>(u_begin / a.rtiles);
+        int rt = static_cast<int>(u_begin % a.rtiles);
+        const int nunits = static_cast<int>(u_end - u_begin);
+        const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(2 * grp * TILE);
+        auto wait_full = [&](int t) {
+            const long long cw_ = (kStats && a.stats) ? clock64() : 0;
+            sm100::mbar_wait(tfull + 2 * grp + (t & 1), static_cast<uint32_t>((t >> 1) & 1));
+            if (kStats && a.stats) st_cyc_wait += clock64() - cw_;
+            sm100::tc_fence_after();
+        };
+        auto release = [&](int t) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + (t & 1));
+        };
+
+        // Software pipeline over 32-column chunks, one TMEM load in flight
+        // (tcgen05.wait::ld waits for all): the load of chunk c+1 -- chunk 0
+        // of the next tile after chunk 3 -- overlaps the scan of chunk c.
+        uint32_t ra[32], rb[32];
+        if (a.mode != 2 && nunits > 0) {
+            wait_full(0);
+            sm100::tmem_ld_32x32b_x32(tlane, ra);
+            sm100::tmem_ld_wait();
+        }
+#define KNN_SCAN_REGS(rr, colb)                                                                  \
+    do {                                                                                         \
+        float v_[32];                                                                            \
+        _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
+        if (!a.fold) add_rnorm(v_, a.rnorm + (colb));                                            \
+        KNN_SCAN_CHUNK(v_, colb);                                                                \
+    } while (0)
+        for (int t = 0; t < nunits; ++t) {
+            if (p != cur_p) {
+                if (cur_p >= 0) {
+                    KNN_DRAIN();
+                    KNN_FLUSH();
+                }
+                cur_p = p;
+                const int qt = 2 * p + grp;
+                q = static_cast<int64_t>(qt) * TILE + row;
+                const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
+                part = static_cast<int64_t>(qt) * a.S_max + slot;
+                const int64_t lq = (part * TILE + row) * a.CG;
+                lvb = a.log_v + 2 * lq;
+                lhb = a.log_h + lq;
+                ln = 0;
+                qc = load_consts(a, q);
+                L.reset();
+                T = kInf;
+                tg_pref = __ldcg(a.tglob + q);
+                Tf = dec_or_inf(tg_pref);
+                sgp = sg0;
+            }
+            const int col_base = rt * TILE;
+            const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
+            if (a.mode == 2) {
+                wait_full(t);
+                release(t);
+            } else {
+                sm100::tmem_ld_32x32b_x32(taddr + 32, rb);
+                KNN_SCAN_REGS(ra, col_base);
+                sm100::tmem_ld_wait();
+                sm100::tmem_ld_32x32b_x32(taddr + 64, ra);
+                KNN_SCAN_REGS(rb, col_base + 32);
+                sm100::tmem_ld_wait();
+                sm100::tmem_ld_32x32b_x32(taddr + 96, rb);
+                KNN_SCAN_REGS(ra, col_base + 64);
+                sm100::tmem_ld_wait();
+                release(t);  // all four chunks of tile t are in registers
+                KNN_SCAN_REGS(rb, col_base + 96);
+                // drain after the release, so the MMA never waits on the list
+                if (__any_sync(0xffffffffu, sgp - sg0 >= static_cast<uint32_t>(a.drain_at * EPI_THREADS * 4)))
+                    KNN_DRAIN();
+                if (t + 1 < nunits) {
+                    wait_full(t + 1);
+                    sm100::tmem_ld_32x32b_x32(tlane + static_cast<uint32_t>(((t + 1) & 1) * TILE), ra);
+                    sm100::tmem_ld_wait();
+                }
+            }
+            if (++rt == a.rtiles) {
+                rt = 0;
+                ++p;
+            }
+        }
+#undef KNN_SCAN_REGS
+        if (cur_p >= 0) {
+            KNN_DRAIN();
+            KNN_FLUSH();
+        }
+        if (kStats && a.stats) {
+            const unsigned long long lg = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(ln));
+            if (lane == 0) {
+                atomicAdd(a.stats + 0, lg);
+                atomicAdd(a.stats + 1, st_drains);
+                atomicAdd(a.stats + 2, st_rounds);
+                atomicAdd(a.stats + 3, lg);
+                atomicAdd(a.stats + 4, static_cast<unsigned long long>(nunits));
+                atomicAdd(a.stats + 5, static_cast<unsigned long long>(st_cyc_drain));
+                atomicAdd(a.stats + 6, static_cast<unsigned long long>(st_cyc_wait));
+                atomicAdd(a.stats + 7, static_cast<unsigned long long>(clock64() - st_cyc0));
+            }
+        }
+#undef KNN_SCAN_CHUNK
+#undef KNN_DRAIN
+#undef KNN_FLUSH
+    }
+
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, 512);
+    }
+}
+
+// Large k (k > 32): one filter pass with a FIXED per-query threshold.  Each
+// segment starts with W seed units (reference tiles spread over the pair's
+// whole reference range, filter_fixed_kernel only): every group minimum of
+// the seed goes into a 32-entry list and T0 = thresh(list[seed_rank-1]) is an
+// estimate of thresh(A_(c*k)).  The main units then log every value A <= T0
+// (compact {A, index} records, predicated stores).  T0 is only an estimate;
+// the selection kernel certifies it (at least k logged values and
+// thresh(A_(k)) <= T0, no log overflow) and sends the rest to the exact path.
+template <int DUMMY>
+__global__ void __launch_bounds__(THREADS, 1)
+    filter_fixed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                        FilterArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int KBB = a.KB * 16384;
+    unsigned char* As = base;
+    unsigned char* Bs = base + 2 * KBB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + a.stages * KBB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + a.stages;
+    uint64_t* a_full = bars + 2 * a.stages;
+    uint64_t* a_empty = a_full + 1;
+    uint64_t* tfull = a_full + 2;
+    uint64_t* tempty = tfull + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int64_t u_begin = unit_start(a.U, a.G, cta);
+    const int64_t u_end = unit_start(a.U, a.G, cta + 1);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.stages; ++s) {
+            sm100::mbar_init(full + s, 1);
+            sm100::mbar_init(empty + s, 2);
+        }
+        sm100::mbar_init(a_full, 1);
+        sm100::mbar_init(a_empty, 2);
+        for (int b = 0; b < 4; ++b) {
+            sm100::mbar_init(tfull + b, 1);
+            sm100::mbar_init(tempty + b, 4);
+        }
+        sm100::fence_mbar_init();
+    }
+    if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
+    const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
+    if (warp == 0) {
+        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, a.W);
+    } else if (warp == 1) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W, 0);
+    } else if (warp == 3) {
+        if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W, 1);
+    } else if (warp >= 4) {
+        sm100::reg_alloc<EPI_REGS>();
+        const int ew = warp - 4;
+        const int grp = ew >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>(2 * grp * TILE);
+        RegList<32> S;  // seed: the 32 smallest seed group minima
+        S.reset();
+        float T0 = kInf;
+        Consts qc{};
+        int64_t q = 0, part = 0;
+        float2* vlp = nullptr;
+        int ln = 0;
+        int cur_p = -1;
+        bool was_seed = false;
+        int64_t t = 0;
+        UnitSeq sq;
+        sq.init(u_begin, u_end, a.rtiles, a.W, a.seed_off);
+        auto finish = [&]() {
+            a.log_n[part * TILE + row] = ln;
+        };
+        for (; sq.more(); sq.next(), ++t) {
+            if (sq.p != cur_p) {
+                if (cur_p >= 0) finish();
+                cur_p = sq.p;
+                const int qt = 2 * sq.p + grp;
+                q = static_cast<int64_t>(qt) * TILE + row;
+                const int slot = cta - first_cta_of(static_cast<int64_t>(sq.p) * a.rtiles, a.U, a.G);
+                part = static_cast<int64_t>(qt) * a.S_max + slot;
+                vlp = a.vlog + (part * TILE + row) * a.CV;
+                ln = 0;
+                qc = load_consts(a, q);
+                S.reset();
+                T0 = kInf;
+            }
+            const bool seed = sq.seed();
+            if (!seed && was_seed) {  // seed complete: fix the segment's threshold
+                T0 = thresh(S.kth(a.seed_rank), qc);
+                if (lane < 32) a.t0[q] = T0;  // identical from every CTA of the pair
+            }
+            was_seed = seed;
+            const int b = static_cast<int>(t & 1);
+            sm100::mbar_wait(tfull + 2 * grp + b, static_cast<uint32_t>((t >> 1) & 1));
+            sm100::tc_fence_after();
+            const uint32_t taddr = tlane + static_cast<uint32_t>(b * TILE);
+            const int col_base = sq.tile() * TILE;
+#pragma unroll 1
+            for (int h = 0; h < 4; ++h) {  // 32-column chunks (one TMEM load each)
+                uint32_t r0[32];
+                sm100::tmem_ld_32x32b_x32(taddr + h * 32, r0);
+                sm100::tmem_ld_wait();
+                if (h == 3) {
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
+                }
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
+                const int cb = col_base + h * 32;
+                if (!a.fold) add_rnorm(v, a.rnorm + cb);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float* w = v + 8 * g;
+                    const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
+                    if (seed) {
+                        S.insert(gm);
+                    } else if (__any_sync(0xffffffffu, gm <= T0)) {
+                        const int col = cb + 8 * g;
+                        if (ln + 8 <= a.CV) {  // room for the whole group: 3 instructions per value
+                            float2* const v0 = vlp;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                asm volatile(
+                                    "{\n\t.reg .pred p;\n\t"
+                                    "setp.le.f32 p, %1, %2;\n\t"
+                                    "@p st.global.v2.b32 [%0], {%1, %3};\n\t"
+                                    "@p add.s64 %0, %0, 8;\n\t}"
+                                    : "+l"(vlp)
+                                    : "f"(w[e]), "f"(T0), "r"(col + e)
+                                    : "memory");
+                            ln += static_cast<int>(vlp - v0);
+                            continue;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int room = ln < a.CV ? 1 : 0;
+                            asm volatile(
+                                "{\n\t.reg .pred p, q;\n\t"
+                                "setp.le.f32 p, %0, %1;\n\t"
+                                "setp.ne.and.s32 q, %2, 0, p;\n\t"
+                                "@q st.global.v2.b32 [%3], {%0, %4};\n\t}" ::"f"(w[e]),
+                                "f"(T0), "r"(room), "l"(vlp), "r"(col + e)
+                                : "memory");
+                            const int hit = w[e] <= T0 ? 1 : 0;
+                            vlp += hit;
+                            ln += hit;
+                        }
+                    }
+                }
+            }
+        }
+        if (cur_p >= 0) finish();
+    }
+
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace
+
+void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
+                   int G, size_t smem, cudaStream_t stream) {
+    auto go = [&](auto kern) {
+        KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+        ProfileScope ps(stream, "tc_filter_kernel");
+        kern<<<G, THREADS, smem, stream>>>(tq, tr, fa);
+    };
+    switch (Kq) {
+        case 4: go(filter_kernel<4>); break;
+        case 8: go(filter_kernel<8>); break;
+        case 12: go(filter_kernel<12>); break;
+        case 16: go(filter_kernel<16>); break;
+        case 20: go(filter_kernel<20>); break;
+        case 24: go(filter_kernel<24>); break;
+        default: go(filter_kernel<32>); break;
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
+                         int G, size_t smem, cudaStream_t stream) {
+    KNN_CUDA_CHECK(cudaFuncSetAttribute(filter_fixed_kernel<0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    {
+        ProfileScope ps(stream, "tc_filter_fixed_kernel");
+        filter_fixed_kernel<0><<<G, THREADS, smem, stream>>>(tq, tr, fa);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+}  // namespace tp
+}  // namespace knnb200

@@ -1,0 +1,264 @@
+// tensor_rerank.cu -- the small-k exact re-rank (warp per query: bound from
+// the union of the part lists, certificate, candidates from the group log,
+// exact FP32 keys, exact top-k) and the gather / scatter of the host-driven
+// fallback.  DESIGN.md sec. 3.2 step 3-4.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "profile.cuh"
+#include "sm100.cuh"
+#include "tensor_internal.cuh"
+#include "warp_list.cuh"
+
+namespace knnb200 {
+namespace tp {
+
+namespace {
+
+// Warp per query.  (1) A_bound = k-th smallest of the union of the parts'
+// bound lists (rank counting over the compacted lists); tau = thresh(A_bound).
+// (2) Certificate: no part's group log overflowed, so every reference with
+// A <= tau is in a log (every filter bound was >= tau).  (3) Candidates =
+// logged values <= tau; their exact FP32 keys (key_step<kL2>, bitwise the
+// exact kernel's arithmetic); (4) exact top-k by (key, index) rank counting.
+__global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * RR_WARPS + warp;
+    if (q >= a.n) return;
+    const int k = a.k;
+    const int Kq = a.Kq;
+    const int parts = a.S_max;  // <= 32 (checked on the host)
+    const int span = parts * Kq;
+    unsigned char* wb = smem_raw + static_cast<size_t>(warp) * rr_warp_bytes(span, k);
+    float* sv = reinterpret_cast<float*>(wb);                 // [span] compacted bound lists
+    float* ck = sv + span;                                     // [RR_CAND] exact keys
+    int* ci = reinterpret_cast<int*>(ck + RR_CAND);            // [RR_CAND] reference indices
+    float* fk = reinterpret_cast<float*>(ci + RR_CAND);        // [k] result keys
+    int64_t* fi = reinterpret_cast<int64_t*>(
+        wb + ((static_cast<size_t>(span) * 4 + RR_CAND * 8 + static_cast<size_t>(k) * 4 + 15) / 16) * 16);
+
+    const int qt = static_cast<int>(q / TILE);
+    const int row = static_cast<int>(q % TILE);
+    const int64_t p0 = static_cast<int64_t>(qt) * parts;
+
+    // Every step below issues its loads for the whole query at once (one
+    // memory round trip per step): the kernel is latency-bound per warp.
+    // part slots written for this pair: one per CTA whose unit range touches it
+    const int pair = qt >> 1;
+    const int nslots = a.f.pair_slots[pair];
+    int cnt = 0, nlog = 0;
+    if (lane < nslots) {
+        cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
+        nlog = a.f.log_n[(p0 + lane) * TILE + row];
+    }
+    const Consts qc = load_consts(a.f, q);
+    // 0. all bound lists, compacted: list p's entries go to [excl_p, excl_p + cnt_p)
+    int cincl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+        if (lane >= o) cincl += y;
+    }
+    const int L = __shfl_sync(0xffffffffu, cincl, 31);
+    for (int p = 0; p < nslots; ++p) {  // a list holds <= Kq <= 32 entries
+        const int cp = __shfl_sync(0xffffffffu, cnt, p);
+        const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+        if (lane < cp) sv[ep + lane] = a.f.part_A[((p0 + p) * Kq + lane) * TILE + row];
+    }
+    __syncwarp();
+
+    // 1. k-th smallest (value, position) of the compacted lists.  Each list is
+    //    sorted, so an entry's rank is its own position plus, per other list,
+    //    a binary search: entries <= v of earlier lists, < v of later ones.
+    float B = kInf;
+    if (L >= k) {
+        for (int x0 = 0; x0 < L; x0 += 32) {  // warp-uniform trip count (shuffles inside)
+            const int x = x0 + lane;
+            const bool valid = x < L;
+            const float v = valid ? sv[x] : kInf;
+            int px = 0;
+            for (int p = 1; p < nslots; ++p)
+                if (x >= __shfl_sync(0xffffffffu, cincl, p - 1)) px = p;
+            int rank = 0;
+            for (int p = 0; p < nslots; ++p) {
+                const int cp = __shfl_sync(0xffffffffu, cnt, p);
+                const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+                // first entry of list p that is not "less" than (v, x)
+                int lo = 0, hi = (p == px || !valid) ? 0 : cp;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const float w = sv[ep + mid];
+                    if (p < px ? w <= v : w < v) lo = mid + 1;
+                    else hi = mid;
+                }
+                rank += p == px ? x - ep : lo;
+            }
+            if (valid && rank == k - 1) B = v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
+    }
+    const float tau = thresh(B, qc);
+
+    // 2. certificate
+    bool ok = __all_sync(0xffffffffu, nlog <= a.f.CG) && isfinite(tau);
+
+    // 3. candidates: logged values <= tau.  Heads of every logged group of
+    //    every part (flattened over parts), then the values of the groups whose
+    //    minimum is inside tau, then their values <= tau.
+    int nc = 0;
+    if (ok) {
+        int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
+        int ng = 0;
+        for (int p = 0; p < nslots; ++p) {
+            const int np = __shfl_sync(0xffffffffu, nlog, p);
+            const int base = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG);
+            for (int t0 = 0; t0 < np; t0 += 32) {
+                const int t = t0 + lane;
+                const bool in = t < np && __int_as_float(a.f.log_h[base + t].x) <= tau;
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pos = ng + __popc(bal & ((1u << lane) - 1u));
+                if (in && pos < RR_CAND) gl[pos] = base + t;
+                ng += __popc(bal);
+            }
+        }
+        ok = ng <= RR_CAND;
+        __syncwarp();
+        for (int j0 = 0; ok && j0 < ng; j0 += 32) {
+            const int j = j0 + lane;
+            float w[8];
+            int c0 = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w[e] = kInf;
+            if (j < ng) {
+                const int slot = gl[j];
+                ldg8(reinterpret_cast<const float*>(a.f.log_v + 2 * static_cast<int64_t>(slot)), w);
+                c0 = a.f.log_h[slot].y;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool c = w[e] <= tau;
+                const unsigned bal = __ballot_sync(0xffffffffu, c);
+                const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+                if (c && pos < RR_CAND) ci[pos] = c0 + e;
+                nc += __popc(bal);
+            }
+        }
+        ok = ok && nc <= RR_CAND && nc >= k;  // heavy ties beyond the fast path: exact kernel
+    }
+    if (!ok) {
+        if (lane == 0) {
+            const int slot = atomicAdd(a.fb_count, 1);
+            a.fb_list[slot] = a.fb_offset + static_cast<int>(q);
+        }
+        return;
+    }
+    __syncwarp();
+
+    // 4. exact FP32 keys of the candidates (lane-parallel, fixed coordinate order)
+    const float* qrow = a.Q + q * a.d;
+    for (int c = lane; c < nc; c += 32)
+        ck[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(ci[c]) * a.d, a.d);
+    __syncwarp();
+
+    // 5. exact top-k under the (key, index) order: up to 32 candidates, one
+    //    per lane, by a shuffle bitonic network; more, by rank counting
+    if (nc <= 32) {
+        float kc = lane < nc ? ck[lane] : kInf;
+        int jc = lane < nc ? ci[lane] : 0x7fffffff;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const float pk = __shfl_xor_sync(0xffffffffu, kc, stride);
+                const int pj = __shfl_xor_sync(0xffffffffu, jc, stride);
+                const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+                if (pair_less(pk, pj, kc, jc) == keep_min) {
+                    kc = pk;
+                    jc = pj;
+                }
+            }
+        if (lane < k) {
+            fk[lane] = kc;
+            fi[lane] = jc;
+        }
+    } else {
+        for (int c = lane; c < nc; c += 32) {
+            const float kc = ck[c];
+            const int jc = ci[c];
+            int r = 0;
+            for (int c2 = 0; c2 < nc; ++c2) r += pair_less(ck[c2], ci[c2], kc, jc) ? 1 : 0;
+            if (r < k) {
+                fk[r] = kc;
+                fi[r] = jc;
+            }
+        }
+    }
+    __syncwarp();
+    if (!a.raw_keys) finalize_list_runs(fk, fi, k, lane);
+    for (int t = lane; t < k; t += 32) {
+        a.out[q * k + t] = fk[t];
+        a.out_idx[q * k + t] = a.index_base + fi[t];
+    }
+}
+
+// gather / scatter for the certification fallback
+__global__ void gather_rows_kernel(const float* X, int d, const int* list, int count, float* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(count) * d;
+    if (i >= total) return;
+    const int64_t r = i / d;
+    out[i] = X[static_cast<int64_t>(list[r]) * d + i % d];
+}
+
+__global__ void scatter_rows_kernel(const float* src_d, const int64_t* src_i, const int* list,
+                                    int count, int k, float* out, int64_t* out_idx) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(count) * k) return;
+    const int64_t r = i / k;
+    const int64_t dst = static_cast<int64_t>(list[r]) * k + i % k;
+    out[dst] = src_d[i];
+    out_idx[dst] = src_i[i];
+}
+
+}  // namespace
+
+void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream) {
+    {
+        ProfileScope ps(stream, "rerank_kernel");
+        rerank_kernel<<<static_cast<unsigned>((ra.n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, smem,
+                        stream>>>(ra);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+void launch_gather_rows(const float* X, int d, const int* list, int count, float* out,
+                        cudaStream_t stream) {
+    const int64_t tot = static_cast<int64_t>(count) * d;
+    {
+        ProfileScope ps(stream, "fallback_gather");
+        gather_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(X, d, list,
+                                                                                       count, out);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+void launch_scatter_rows(const float* src_d, const int64_t* src_i, const int* list, int count,
+                         int k, float* out, int64_t* out_idx, cudaStream_t stream) {
+    const int64_t tot = static_cast<int64_t>(count) * k;
+    {
+        ProfileScope ps(stream, "fallback_scatter");
+        scatter_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
+            src_d, src_i, list, count, k, out, out_idx);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+}  // namespace tp
+}  // namespace knnb200

@@ -1,0 +1,339 @@
+// tensor_select.cu -- large-k selection (k > 32): one block per query
+// certifies the fixed threshold, computes the exact FP32 keys of the values
+// inside the bound and sorts them (register/shuffle bitonic network, block
+// radix select).  DESIGN.md sec. 3.3.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "profile.cuh"
+#include "sm100.cuh"
+#include "tensor_internal.cuh"
+#include "warp_list.cuh"
+
+namespace knnb200 {
+namespace tp {
+
+namespace {
+
+// Large-k selection, one 256-thread block per query: gather the query's
+// logged {A, index} values, bitonic-sort them by A, A_(k) = k-th; certify
+// (>= k logged, no overflow, thresh(A_(k)) <= T0); exact FP32 keys of every
+// value <= thresh(A_(k)); bitonic sort by (key, index); top k.
+#ifndef KNN_DBG_LARGE
+#define KNN_DBG_LARGE 0
+#endif
+
+// Bitonic sort of N (power of two) (key, index) pairs in shared memory under
+// the (key, index) order, by `nthreads` threads (32: one warp, no block
+// barriers; or the whole block).  Thread t holds elements t E .. t E + E - 1 in
+// registers (E = N / nthreads): strides below E are register swaps, strides
+// below 32 E are lane shuffles, and only the strides that cross warps go
+// through shared memory (one barrier each) -- 18 barriers at N = 2048 where the
+// all-shared-memory network needs 66.
+template <int E>
+__device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) {
+    const int t = threadIdx.x;
+    const bool active = t < nthreads;
+    const int W = 32 * E;  // elements per warp
+    float rk[E];
+    int ri[E];
+    __syncthreads();  // the caller's writes of key/idx are visible
+    if (active)
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            rk[j] = key[t * E + j];
+            ri[j] = idx[t * E + j];
+        }
+    for (int size = 2; size <= N; size <<= 1) {
+        int stride = size >> 1;
+        if (stride >= W) {  // cross-warp strides (nthreads > 32 only)
+            __syncthreads();  // everyone is done reading the previous shared phase
+            if (active)
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    key[t * E + j] = rk[j];
+                    idx[t * E + j] = ri[j];
+                }
+            for (; stride >= W; stride >>= 1) {
+                __syncthreads();
+                for (int i = t; i < (N >> 1); i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1));
+                    const int hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const float ka = key[lo], kb = key[hi];
+                    const int ia = idx[lo], ib = idx[hi];
+                    if (pair_less(kb, ib, ka, ia) == up) {
+                        key[lo] = kb;
+                        key[hi] = ka;
+                        idx[lo] = ib;
+                        idx[hi] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+            if (active)
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    rk[j] = key[t * E + j];
+                    ri[j] = idx[t * E + j];
+                }
+        }
+        if (!active) continue;
+        for (; stride >= E; stride >>= 1) {  // partner in lane ^ (stride / E), same slot
+            const int lm = stride / E;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const float pk = __shfl_xor_sync(0xffffffffu, rk[j], lm);
+                const int pi = __shfl_xor_sync(0xffffffffu, ri[j], lm);
+                const int e = t * E + j;
+                const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
+                const bool p_less = pair_less(pk, pi, rk[j], ri[j]);
+                if (p_less == keep_min) {
+                    rk[j] = pk;
+                    ri[j] = pi;
+                }
+            }
+        }
+#pragma unroll
+        for (int s = E / 2; s > 0; s >>= 1) {  // partner in this thread
+            if (s > stride) continue;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                if (j & s) continue;
+                const bool up = ((t * E + j) & size) == 0;
+                if (pair_less(rk[j + s], ri[j + s], rk[j], ri[j]) == up) {
+                    const float tk = rk[j];
+                    const int ti = ri[j];
+                    rk[j] = rk[j + s];
+                    ri[j] = ri[j + s];
+                    rk[j + s] = tk;
+                    ri[j + s] = ti;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (active)
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            key[t * E + j] = rk[j];
+            idx[t * E + j] = ri[j];
+        }
+    __syncthreads();
+}
+
+// N (power of two, 32 <= N <= 16 * blockDim.x) pairs by the whole block:
+// one element per thread up to N = blockDim.x, then N / blockDim.x.
+__device__ void bitonic_sort_kv(float* key, int* idx, int N) {
+    const int bd = static_cast<int>(blockDim.x);
+    if (N <= bd) {
+        bitonic_sort_kv_regs<1>(key, idx, N, N);
+        return;
+    }
+    switch (N / bd) {
+        case 2: bitonic_sort_kv_regs<2>(key, idx, N, bd); break;
+        case 4: bitonic_sort_kv_regs<4>(key, idx, N, bd); break;
+        case 8: bitonic_sort_kv_regs<8>(key, idx, N, bd); break;
+        default: bitonic_sort_kv_regs<16>(key, idx, N, bd); break;
+    }
+}
+
+// k-th smallest (1-based) of x[0..n) (finite floats), block-wide radix select
+// on enc() bits, most significant digit first.  hist: 256 shared counters.
+__device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist, int* scratch) {
+    unsigned prefix = 0, mask = 0;
+    int want = k;  // rank still to find among keys matching prefix
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
+        __syncthreads();
+        // warp-aggregated increments: the leading digits of nearby keys
+        // coincide, so plain atomics would serialise on one or two bins
+        for (int e0 = 0; e0 < n; e0 += blockDim.x) {
+            const int e = e0 + threadIdx.x;
+            int bin = -1;
+            if (e < n) {
+                const unsigned u = enc(x[e]);
+                if ((u & mask) == prefix) bin = static_cast<int>((u >> shift) & 255u);
+            }
+            const unsigned same = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && (__ffs(same) - 1) == (threadIdx.x & 31))
+                atomicAdd(hist + bin, static_cast<unsigned>(__popc(same)));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // warp 0: the bin holding rank `want` (8 bins per lane)
+            const int l = threadIdx.x;
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = hist[8 * l + j];
+                tot += c[j];
+            }
+            unsigned incl = tot;  // inclusive prefix over lanes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (l >= o) incl += y;
+            }
+            const unsigned excl = incl - tot;
+            if (excl < static_cast<unsigned>(want) && static_cast<unsigned>(want) <= incl) {
+                unsigned acc = excl;
+                int j = 0;
+                for (; j < 7; ++j) {
+                    if (acc + c[j] >= static_cast<unsigned>(want)) break;
+                    acc += c[j];
+                }
+                scratch[0] = 8 * l + j;
+                scratch[1] = want - static_cast<int>(acc);
+            }
+        }
+        __syncthreads();
+        const unsigned b = static_cast<unsigned>(scratch[0]);
+        want = scratch[1];
+        prefix |= b << shift;
+        mask |= 255u << shift;
+        __syncthreads();
+    }
+    return dec(prefix);
+}
+
+// NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
+// capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
+template <int NT>
+__global__ void __launch_bounds__(NT) select_large_kernel(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
+    int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
+    __shared__ int s_off[33];
+    __shared__ int s_cnt;
+    __shared__ int s_sel[2];
+    __shared__ unsigned s_hist[256];
+    const int64_t q = blockIdx.x;
+    const int qt = static_cast<int>(q / TILE), row = static_cast<int>(q % TILE);
+    const int64_t p0 = static_cast<int64_t>(qt) * a.S_max;
+    const int k = a.k;
+    if (threadIdx.x == 0) {
+        int off = 0;
+        bool over = false;
+        const int pair = qt >> 1;  // slots written: one per CTA touching the pair
+        const int nslots = a.f.pair_slots[pair];
+        for (int p = 0; p < a.S_max; ++p) {
+            const int np = p < nslots ? a.f.log_n[(p0 + p) * TILE + row] : 0;
+            over |= np > a.f.CV;
+            s_off[p] = off;
+            off += min(np, a.f.CV);
+        }
+        s_off[a.S_max] = off;
+        s_cnt = over ? -1 : off;
+    }
+    __syncthreads();
+    const int total = s_cnt;
+    const float T0 = a.f.t0[q];
+    bool ok = total >= k && total <= a.NC;
+    float tau = kInf;
+    int nc = 0;
+    if (ok) {
+        for (int p = 0; p < a.S_max; ++p) {
+            const int o = s_off[p], np = s_off[p + 1] - o;
+            const float2* src = a.f.vlog + ((p0 + p) * TILE + row) * a.f.CV;
+            for (int e = threadIdx.x; e < np; e += blockDim.x) {
+                const float2 r = src[e];
+                sk[o + e] = r.x;
+                si[o + e] = __float_as_int(r.y);
+            }
+        }
+        __syncthreads();
+        // A_(k) by radix select on the order-preserving key bits (4 x 8-bit
+        // digits, block histograms), no sort
+        const float ak = block_kth_smallest(sk, total, k, s_hist, s_sel);
+        const Consts qc = load_consts(a.f, q);
+        tau = thresh(ak, qc);
+        ok = tau <= T0;  // every reference with A <= tau was logged
+        if (ok) {
+            // compact the candidates (A <= tau) to the front, any order
+            if (threadIdx.x == 0) s_cnt = 0;
+            __syncthreads();
+            int mine[16];  // total <= NC <= 16 * NT: a thread owns <= 16 entries
+            int nm = 0;
+            for (int e = threadIdx.x; e < total; e += blockDim.x)
+                if (sk[e] <= tau) mine[nm++] = si[e];
+            __syncthreads();
+            const int base = atomicAdd(&s_cnt, nm);
+            for (int j = 0; j < nm; ++j) si[base + j] = mine[j];
+            __syncthreads();
+            nc = s_cnt;
+        }
+    }
+    if (!ok) {
+        if (threadIdx.x == 0) {
+            const int slot = atomicAdd(a.fb_count, 1);
+            a.fb_list[slot] = a.fb_offset + static_cast<int>(q);
+            if (KNN_DBG_LARGE && slot < 8)
+                printf("[select_large] q=%lld total=%d k=%d NC=%d tau=%g T0=%g nc=%d\n",
+                       static_cast<long long>(q), total, k, a.NC, tau, T0, nc);
+        }
+        return;
+    }
+    // exact keys of the nc candidates (their indices are si[0..nc))
+    const float* qrow = a.Q + q * a.d;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x)
+        sk[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(si[c]) * a.d, a.d);
+    int N2 = 32;
+    while (N2 < nc) N2 <<= 1;
+    for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
+        sk[e] = kInf;
+        si[e] = 0x7fffffff;
+    }
+    bitonic_sort_kv(sk, si, N2);
+    // finalize: sqrt, then equal reported distances in ascending index order
+    if (!a.raw_keys) {
+        for (int t = threadIdx.x; t < k; t += blockDim.x) sk[t] = __fsqrt_rn(sk[t]);
+        __syncthreads();
+        // equal reported distances in ascending index order: each run of
+        // equal distances (keys were ascending, so runs are contiguous and
+        // short) is insertion-sorted by the thread owning its first slot
+        for (int t = threadIdx.x; t < k; t += blockDim.x) {
+            if (t > 0 && sk[t - 1] == sk[t]) continue;
+            int e = t + 1;
+            while (e < k && sk[e] == sk[t]) ++e;
+            for (int x = t + 1; x < e; ++x) {
+                const int j = si[x];
+                int u = x;
+                while (u > t && si[u - 1] > j) {
+                    si[u] = si[u - 1];
+                    --u;
+                }
+                si[u] = j;
+            }
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        a.out[q * k + t] = sk[t];
+        a.out_idx[q * k + t] = a.index_base + si[t];
+    }
+}
+
+}  // namespace
+
+void launch_select_large(const LargeArgs& la, cudaStream_t stream) {
+    const size_t smem = static_cast<size_t>(la.NC) * 8;
+    const int NC = la.NC;
+    const int nt = NC <= 16 * 64 ? 64 : NC <= 16 * 128 ? 128 : NC <= 16 * 256 ? 256 : LK_THREADS;
+    auto sel = nt == 64    ? select_large_kernel<64>
+               : nt == 128 ? select_large_kernel<128>
+               : nt == 256 ? select_large_kernel<256> : select_large_kernel<LK_THREADS>;
+    KNN_CUDA_CHECK(cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    {
+        ProfileScope ps(stream, "select_large_kernel");
+        sel<<<static_cast<unsigned>(la.n), nt, smem, stream>>>(la);
+    }
+    KNN_LAUNCH_CHECK();
+}
+
+}  // namespace tp
+}  // namespace knnb200
