@@ -160,6 +160,9 @@ KNN_B200_API void knn_b200_reset_launch_count(void);
  * collect() synchronizes, writes newline-separated kernel names, total ms and
  * launch counts per kernel, resets, and returns the number of kernels. */
 KNN_B200_API void knn_b200_profile_enable(int on);
+/* Restrict the events to launches whose name starts with `prefix` (NULL or ""
+ * = every launch): fewer events, less perturbation of the timed region. */
+KNN_B200_API void knn_b200_profile_only(const char *prefix);
 KNN_B200_API int knn_b200_profile_collect(char *names, size_t names_len, double *ms,
                                           uint64_t *counts, int max_kernels);
 

@@ -39,7 +39,7 @@ EXPORTS = [
     "knn_b200_search_device", "knn_b200_index_create", "knn_b200_index_create_device",
     "knn_b200_index_search", "knn_b200_index_search_device", "knn_b200_index_destroy",
     "knn_b200_merge_device", "knn_b200_launch_count", "knn_b200_reset_launch_count",
-    "knn_b200_profile_enable", "knn_b200_profile_collect", "knn_b200_fill_uniform_device",
+    "knn_b200_profile_enable", "knn_b200_profile_only", "knn_b200_profile_collect", "knn_b200_fill_uniform_device",
     "knn_b200_last_fallback_count", "knn_b200_debug_mma_probe",
 ]
 
@@ -98,6 +98,7 @@ def library() -> C.CDLL:
     lib.knn_b200_merge_device.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp]
     lib.knn_b200_launch_count.restype = C.c_uint64
     lib.knn_b200_profile_enable.argtypes = [C.c_int]
+    lib.knn_b200_profile_only.argtypes = [C.c_char_p]
     lib.knn_b200_profile_collect.restype = C.c_int
     lib.knn_b200_profile_collect.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_double),
                                              C.POINTER(C.c_uint64), C.c_int]
@@ -126,8 +127,10 @@ def last_fallback_count(device: int = -1) -> int:
     return int(library().knn_b200_last_fallback_count(device))
 
 
-def profile_enable(on: bool = True) -> None:
-    """Bracket every engine launch on this thread with CUDA events."""
+def profile_enable(on: bool = True, only: str = "") -> None:
+    """Bracket every engine launch on this thread (or only those whose name
+    starts with `only`) with CUDA events."""
+    library().knn_b200_profile_only(only.encode())
     library().knn_b200_profile_enable(int(bool(on)))
 
 

@@ -22,6 +22,7 @@ struct Rec {
     cudaEvent_t a, b;
 };
 thread_local bool g_profile = false;
+thread_local std::string g_only;  // name prefix filter ("" = all)
 thread_local std::vector<Rec> g_recs;
 thread_local std::vector<cudaEvent_t> g_pool;
 
@@ -39,6 +40,7 @@ cudaEvent_t take_event() {
 
 ProfileScope::ProfileScope(cudaStream_t s, const char* name) : stream_(s), name_(name) {
     if (!g_profile) return;
+    if (!g_only.empty() && std::strncmp(name, g_only.c_str(), g_only.size()) != 0) return;
     a_ = take_event();
     b_ = take_event();
     KNN_CUDA_CHECK(cudaEventRecord(static_cast<cudaEvent_t>(a_), stream_));
@@ -71,6 +73,8 @@ using namespace knnb200;
 extern "C" {
 
 void knn_b200_profile_enable(int on) { g_profile = on != 0; }
+
+void knn_b200_profile_only(const char* prefix) { g_only = prefix ? prefix : ""; }
 
 int knn_b200_profile_collect(char* names, size_t names_len, double* ms, uint64_t* counts,
                              int max_kernels) {
