@@ -1,0 +1,25 @@
+"""Dev tool (GPU, under compute-sanitizer): small searches over every kernel
+family -- exact (3 metrics, list variants, stream-K slots), tensor small/large
+k, device fallback, Mahalanobis whitening, merge."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_0804_1448_b200 as knn
+rng = np.random.default_rng(5)
+def run(n, m, d, k, metric=knn.EUCLIDEAN, path=knn.PATH_AUTO, R=None):
+    Q = rng.random((n, d), dtype=np.float32)
+    R = rng.random((m, d), dtype=np.float32) if R is None else R
+    t = knn.bf_knn(Q, R, k, knn.Metric(metric), config=knn.BfConfig(path=path))
+    assert (t.index >= 0).all()
+for metric in (knn.EUCLIDEAN, knn.MANHATTAN, knn.CHEBYSHEV):
+    for k in (1, 33, 129, 300):
+        run(150, 3000, 37, k, metric, knn.PATH_EXACT)
+run(300, 5000, 24, 20, path=knn.PATH_TENSOR)
+run(300, 5000, 24, 100, path=knn.PATH_TENSOR)
+run(200, 3000, 96, 1024, path=knn.PATH_TENSOR)
+dup = np.repeat(rng.random((1, 16), dtype=np.float32), 9000, axis=0)
+run(50, 9000, 16, 20, path=knn.PATH_TENSOR, R=dup)
+M = np.eye(8) * 2.0
+Q = rng.random((40, 8), dtype=np.float32); R = rng.random((900, 8), dtype=np.float32)
+knn.bf_knn(Q, R, 5, knn.Metric.mahalanobis(8, M.ravel()))
+print("sanitize smoke ok", flush=True)
