@@ -423,7 +423,7 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
                                           MX_WARPS * static_cast<size_t>(a.k) * 8
                                     : 0;
     const unsigned grid = static_cast<unsigned>(
-        std::max<int64_t>(1, std::min<int64_t>((a.n + MX_WARPS - 1) / MX_WARPS, 16 * kSmCount)));
+        std::max<int64_t>(1, std::min<int64_t>((a.n + MX_WARPS - 1) / MX_WARPS, 4 * kSmCount)));
     ProfileScope ps(stream, "merge_exact_kernel");
     if (mx_smem) {
         KNN_CUDA_CHECK(cudaFuncSetAttribute(merge_exact_kernel<M, true>,
