@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* GB = reinterpret_cast<float*>(Bs + a.stages * KBB);        // [CAP][512] group minima
     uint64_t* sT = reinterpret_cast<uint64_t*>(GB + CAP * EPI_THREADS);  // [2][128] tagged bounds
     uint64_t* sP = sT + 2 * TILE;                                       // [2][2][128] tagged kp-th
-    uint64_t* bars = sP + 4 * TILE;
+    float* RN = reinterpret_cast<float*>(sP + 4 * TILE);  // [EPI_WARPS][128] staged ||r~||^2 (no-fold)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(RN + EPI_WARPS * TILE);
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
     uint64_t* a_full = bars + 2 * a.stages;
@@ -194,11 +195,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             sm100::tmem_ld_32x32b_x32(tlane, ra);
             sm100::tmem_ld_wait();
         }
+        // no-fold layouts: the unit's 128 reference norms are staged in this
+        // warp's smem slot (one 16-B load per lane, issued a unit ahead) and
+        // read back as broadcasts, instead of 8 global loads per chunk
+        float* const rnw = RN + ew * TILE;
+        float4 rn_nx = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!a.fold && nunits > 0)
+            rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + rt * TILE) + lane);
 #define KNN_SCAN_REGS(rr, colb)                                                                  \
     do {                                                                                         \
         float v_[32];                                                                            \
         _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
-        if (!a.fold) add_rnorm(v_, a.rnorm + (colb));                                            \
+        if (!a.fold) add_rnorm_smem(v_, rnw + ((colb) - col_base));                              \
         KNN_SCAN_CHUNK(v_, colb);                                                                \
     } while (0)
         for (int t = 0; t < nunits; ++t) {
@@ -225,6 +233,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const int col_base = rt * TILE;
             const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
+            if (!a.fold) {  // stage this unit's norms, prefetch the next unit's
+                __syncwarp();
+                reinterpret_cast<float4*>(rnw)[lane] = rn_nx;
+                __syncwarp();
+                if (t + 1 < nunits) {
+                    const int nrt = rt + 1 == a.rtiles ? 0 : rt + 1;
+                    rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + nrt * TILE) + lane);
+                }
+            }
             if (a.mode == 2) {
                 wait_full(t);
                 release(t);

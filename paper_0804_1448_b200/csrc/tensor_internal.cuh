@@ -192,11 +192,24 @@ __device__ __forceinline__ void push_group_off(float gm, float tf, uint32_t& sgp
 }
 
 // no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~
+// (all lanes read the same addresses -- broadcasts).  Global (read-only path)
+// or shared-memory source.
 __device__ __forceinline__ void add_rnorm(float (&v)[32], const float* rn) {
     const float4* nr = reinterpret_cast<const float4*>(rn);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const float4 w = __ldg(nr + j);
+        v[4 * j] += w.x;
+        v[4 * j + 1] += w.y;
+        v[4 * j + 2] += w.z;
+        v[4 * j + 3] += w.w;
+    }
+}
+__device__ __forceinline__ void add_rnorm_smem(float (&v)[32], const float* rn) {
+    const float4* nr = reinterpret_cast<const float4*>(rn);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float4 w = nr[j];
         v[4 * j] += w.x;
         v[4 * j + 1] += w.y;
         v[4 * j + 2] += w.z;
@@ -481,7 +494,8 @@ inline Layout layout_for(int d, int k) {
         ncol = L.d16;
     }
     const int kb_fold = (kfold + 63) / 64;
-    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 + 6 * TILE * 8;
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 + 6 * TILE * 8 +
+                       static_cast<size_t>(EPI_WARPS) * TILE * 4;  // + staged reference norms
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
     auto stages_for = [&](int KB) {
         const size_t per = static_cast<size_t>(KB) * 16384;
