@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int KBB = a.KB * 16384;
     unsigned char* As = base;
     unsigned char* Bs = base + 2 * KBB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + a.stages * KBB);
+    float* RN = reinterpret_cast<float*>(Bs + a.stages * KBB);  // [EPI_WARPS][128] staged norms
+    uint64_t* bars = reinterpret_cast<uint64_t*>(RN + EPI_WARPS * TILE);
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
     uint64_t* a_full = bars + 2 * a.stages;
@@ -381,6 +382,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         int64_t t = 0;
         UnitSeq sq;
         sq.init(u_begin, u_end, a.rtiles, a.W, a.seed_off);
+        // no-fold layouts: reference norms staged per unit (see filter_kernel)
+        float* const rnw = RN + (warp - 4) * TILE;
+        float4 rn_nx = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!a.fold && sq.more())
+            rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + sq.tile() * TILE) + lane);
         auto finish = [&]() {
             a.log_n[part * TILE + row] = ln;
         };
@@ -409,6 +415,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             sm100::tc_fence_after();
             const uint32_t taddr = tlane + static_cast<uint32_t>(b * TILE);
             const int col_base = sq.tile() * TILE;
+            if (!a.fold) {
+                __syncwarp();
+                reinterpret_cast<float4*>(rnw)[lane] = rn_nx;
+                __syncwarp();
+                UnitSeq nx = sq;
+                nx.next();
+                if (nx.more())
+                    rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + nx.tile() * TILE) + lane);
+            }
 #pragma unroll 1
             for (int h = 0; h < 4; ++h) {  // 32-column chunks (one TMEM load each)
                 uint32_t r0[32];
@@ -423,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
                 const int cb = col_base + h * 32;
-                if (!a.fold) add_rnorm(v, a.rnorm + cb);
+                if (!a.fold) add_rnorm_smem(v, rnw + h * 32);
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const float* w = v + 8 * g;

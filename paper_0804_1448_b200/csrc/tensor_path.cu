@@ -269,9 +269,15 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         fa.t0 = t0;
         fa.vlog = vlog;
         fa.CV = CV;
-        const size_t smem_fixed = 1024 + 512 + static_cast<size_t>(L.KB) * 16384 *
-                                                   (2 + std::min(L.stages + 2, 6));
-        const int stages_fixed = std::min(L.stages + 2, 6);
+        // no epilogue buffers here: more stages, minus the staged reference norms
+        int stages_fixed = std::min(L.stages + 2, 6);
+        auto fixed_bytes = [&](int st) {
+            return 1024 + 512 + static_cast<size_t>(EPI_WARPS) * TILE * 4 +
+                   static_cast<size_t>(L.KB) * 16384 * (2 + st);
+        };
+        while (stages_fixed > 2 && fixed_bytes(stages_fixed) > static_cast<size_t>(SMEM_LIMIT))
+            --stages_fixed;
+        const size_t smem_fixed = fixed_bytes(stages_fixed);
         fa.stages = stages_fixed;
         launch_filter_fixed(tq, tr, fa, G, smem_fixed, stream);
         LargeArgs la{};
