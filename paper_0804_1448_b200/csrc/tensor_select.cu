@@ -203,7 +203,7 @@ __device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist
 // NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
 // capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
 template <int NT>
-__global__ void __launch_bounds__(NT) select_large_kernel(LargeArgs a) {
+__global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(LargeArgs a) {  // <= 64 registers
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
     int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
