@@ -1,4 +1,5 @@
-// knn_b200_cli -- the reference CLI's `search` subcommand on the B200 engine.
+// knn_b200_cli -- the reference CLI's `search` and `bench` subcommands on the
+// B200 engine.
 //
 // Mirrors /root/reference/proj/tools/knn_cli.cpp (run_search, :66-96, and the
 // option table of main, :232-244) and the point/matrix CSV readers of
@@ -10,17 +11,30 @@
 // 2 malformed input file ("error: line N: ..."), 3 contract violation
 // (std::invalid_argument), 1 anything else, 2 for unknown options.
 //
+// `bench` mirrors run_grid / write_report_csv / write_report_json
+// (src/bench.cpp:75-166, 207-232) for the brute-force method: per (n, d) cell
+// uniform points from mt19937_64 seeded derive_seed(seed, n, d, 0 | 1)
+// (include/knn/rng.hpp), bf_knn timed `--reps` times (median; first rep is
+// warm-up from 4 reps on), the time budget, and the report schema
+//   method,n,d,k,seconds,dist_evals,seed
+// `kdt` rows are not available (the kd-tree is outside this engine): asking
+// for them is a contract error (exit 3).
+//
 // Differences a caller can see: the search runs on the GPU in FP32 (distances
 // are printed as the shortest decimal of the FP32 value, so the reference's
 // CLI test fixture prints identically: 0.1 / 0.9 / 1.9), and `--method kdtree`
 // runs the same exact search (the kd-tree reports the same neighbours,
 // test_cli.cpp:70-75); --workers / --chunk-size / --leaf-size are accepted
 // and do not change results.
+#include <algorithm>
 #include <charconv>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
 #include <iostream>
+#include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -205,14 +219,164 @@ int run_search(int argc, char** argv) {
     return 0;
 }
 
+// include/knn/rng.hpp: splitmix64, derive_seed, next_unit
+std::uint64_t splitmix64(std::uint64_t& state) {
+    std::uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+std::uint64_t derive_seed(std::uint64_t master, std::uint64_t a, std::uint64_t b, std::uint64_t c) {
+    std::uint64_t state = master;
+    std::uint64_t out = splitmix64(state);
+    state ^= a * 0x9e3779b97f4a7c15ULL;
+    out ^= splitmix64(state);
+    state ^= b * 0xbf58476d1ce4e5b9ULL;
+    out ^= splitmix64(state);
+    state ^= c * 0x94d049bb133111ebULL;
+    out ^= splitmix64(state);
+    return out;
+}
+
+knn_b200::PointSet generate_uniform(std::size_t n, std::size_t d, std::uint64_t seed) {
+    std::mt19937_64 gen(seed);  // bench.cpp:39-46
+    std::vector<double> data(n * d);
+    for (double& v : data) v = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+    return knn_b200::PointSet(n, d, std::move(data));
+}
+
+std::vector<std::size_t> parse_list(const std::string& opt, const std::string& v) {
+    std::vector<std::size_t> out;
+    std::size_t start = 0;
+    while (true) {
+        const std::size_t comma = v.find(',', start);
+        out.push_back(parse_number<std::size_t>(opt, v.substr(start, comma - start)));
+        if (comma == std::string::npos) break;
+        start = comma + 1;
+    }
+    return out;
+}
+
+std::vector<std::string> parse_methods(const std::string& v) {  // bench.cpp:27-31 names
+    std::vector<std::string> out;
+    std::size_t start = 0;
+    while (true) {
+        const std::size_t comma = v.find(',', start);
+        std::string name = v.substr(start, comma - start);
+        if (name == "kdtree") name = "kdt";
+        if (name != "bf" && name != "kdt")
+            throw std::invalid_argument("unknown method '" + name + "', expected bf or kdt");
+        out.push_back(name);
+        if (comma == std::string::npos) break;
+        start = comma + 1;
+    }
+    return out;
+}
+
+std::string format_double(double value) {  // csv.cpp:172-176
+    char buf[32];
+    const auto [ptr, ec] = std::to_chars(buf, buf + sizeof(buf), value);
+    return std::string(buf, ptr);
+}
+
+int run_bench(int argc, char** argv) {
+    std::vector<std::size_t> n_values{1200, 2400}, d_values{8, 16, 32, 64, 80, 96};  // default_grid
+    std::string metric = "euclidean", out_path, json_path, methods = "bf";
+    std::size_t k = 20, reps = 3;
+    std::uint64_t seed = 0;
+    double budget = 120.0;
+    for (int i = 2; i < argc; ++i) {
+        const std::string opt = argv[i];
+        if (i + 1 >= argc) throw UsageError(opt + ": missing value");
+        const std::string val = argv[++i];
+        if (opt == "--grid") {
+            if (val != "default") throw UsageError("--grid: the only named grid is 'default'");
+        } else if (opt == "--n-values") n_values = parse_list(opt, val);
+        else if (opt == "--d-values") d_values = parse_list(opt, val);
+        else if (opt == "--methods") methods = val;
+        else if (opt == "--metric") metric = val;
+        else if (opt == "--k") k = parse_number<std::size_t>(opt, val);
+        else if (opt == "--reps") reps = parse_number<std::size_t>(opt, val);
+        else if (opt == "--seed") seed = parse_number<std::uint64_t>(opt, val);
+        else if (opt == "--workers") parse_number<unsigned>(opt, val);
+        else if (opt == "--time-budget") budget = parse_number<double>(opt, val);
+        else if (opt == "--out") out_path = val;
+        else if (opt == "--json") json_path = val;
+        else throw UsageError("The following argument was not expected: " + opt);
+    }
+    for (const std::string& mth : parse_methods(methods))
+        if (mth != "bf")
+            throw std::invalid_argument("method '" + mth +
+                                        "' is not available on the B200 engine (bf only)");
+    if (reps == 0) throw std::invalid_argument("run_grid: repetitions must be >= 1");
+    for (std::size_t n : n_values)
+        if (k > n)
+            throw std::invalid_argument("run_grid: k = " + std::to_string(k) +
+                                        " exceeds cell size n = " + std::to_string(n));
+    const knn_b200::Metric m = parse_metric(metric);
+
+    std::ostringstream csv, json;
+    csv << "method,n,d,k,seconds,dist_evals,seed\n";
+    json << "{\n  \"environment\": \"knn_b200 engine (B200), metric " << metric
+         << ", points uniform [0,1)^d\",\n  \"rows\": [";
+    bool first = true;
+    for (std::size_t n : n_values)
+        for (std::size_t d : d_values) {
+            const knn_b200::PointSet refs = generate_uniform(n, d, derive_seed(seed, n, d, 0));
+            const knn_b200::PointSet queries = generate_uniform(n, d, derive_seed(seed, n, d, 1));
+            knn_b200::BfConfig cfg;
+            cfg.count_distance_evals = true;
+            std::vector<double> times;
+            std::uint64_t evals = 0;
+            bool skipped = false;
+            for (std::size_t rep = 0; rep < reps; ++rep) {
+                knn_b200::SearchStats stats;
+                const auto t0 = std::chrono::steady_clock::now();
+                (void)knn_b200::bf_knn(queries, refs, k, m, cfg, &stats);
+                times.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+                evals = stats.distance_evals;
+                if (rep == 0 && times[0] > budget) {
+                    skipped = true;
+                    break;
+                }
+            }
+            double seconds = NAN;
+            if (!skipped) {
+                std::vector<double> t(times.begin() + (reps >= 4 ? 1 : 0), times.end());
+                std::sort(t.begin(), t.end());
+                const std::size_t mid = t.size() / 2;
+                seconds = t.size() % 2 ? t[mid] : 0.5 * (t[mid - 1] + t[mid]);
+            }
+            std::cerr << "bf n=" << n << " d=" << d << " k=" << k
+                      << (skipped ? " skipped (over time budget)" : " seconds=" + format_double(seconds))
+                      << " dist_evals=" << evals << '\n';
+            csv << "bf," << n << ',' << d << ',' << k << ',' << (skipped ? "NA" : format_double(seconds))
+                << ',' << evals << ',' << seed << '\n';
+            json << (first ? "" : ",") << "\n    {\"method\": \"bf\", \"n\": " << n << ", \"d\": " << d
+                 << ", \"k\": " << k << ", \"dist_evals\": " << evals << ", \"seed\": " << seed
+                 << ", \"skipped\": " << (skipped ? "true" : "false") << ", \"seconds\": "
+                 << (skipped ? "null" : format_double(seconds)) << "}";
+            first = false;
+        }
+    json << "\n  ]\n}\n";
+    write_output(out_path, csv.str());
+    if (!json_path.empty()) write_output(json_path, json.str());
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
-        if (argc < 2 || std::string(argv[1]) != "search")
-            throw UsageError("usage: knn_b200_cli search --ref R.csv --query Q.csv --k K "
-                             "[--metric M] [--method bf|kdtree] [--out OUT.csv]");
-        return run_search(argc, argv);
+        const std::string cmd = argc >= 2 ? argv[1] : "";
+        if (cmd == "search") return run_search(argc, argv);
+        if (cmd == "bench") return run_bench(argc, argv);
+        throw UsageError("usage: knn_b200_cli search --ref R.csv --query Q.csv --k K "
+                         "[--metric M] [--method bf|kdtree] [--out OUT.csv]\n"
+                         "       knn_b200_cli bench [--grid default] [--n-values N,..] "
+                         "[--d-values D,..] [--k K] [--reps R] [--seed S] [--out OUT.csv] "
+                         "[--json OUT.json]");
     } catch (const UsageError& e) {
         std::cerr << "error: " << e.what() << '\n';
         return 2;

@@ -97,3 +97,31 @@ def test_contract_violations_exit_3(cli, tmp_path):
 def test_unknown_flags_are_an_error(cli):
     code, _, _ = run(cli, "search", "--frobnicate", "3")
     assert code != 0
+
+
+@pytest.mark.gpu
+def test_bench_grid_report(cli, tmp_path):
+    """knn-cli bench (bench.cpp:75-166, 207-232) for the bf method: the report
+    schema, one row per (n, d) cell, n*n distance evaluations, JSON twin."""
+    import json
+    out, js = str(tmp_path / "grid.csv"), str(tmp_path / "grid.json")
+    code, _, err = run(cli, "bench", "--n-values", "300,500", "--d-values", "8,16,32", "--k",
+                       "5", "--reps", "2", "--seed", "42", "--out", out, "--json", js)
+    assert code == 0, err
+    lines = open(out).read().strip().split("\n")
+    assert lines[0] == "method,n,d,k,seconds,dist_evals,seed"
+    rows = [r.split(",") for r in lines[1:]]
+    assert [(r[0], int(r[1]), int(r[2])) for r in rows] == [
+        ("bf", n, d) for n in (300, 500) for d in (8, 16, 32)]
+    for r in rows:
+        n = int(r[1])
+        assert int(r[3]) == 5 and float(r[4]) > 0 and int(r[5]) == n * n and r[6] == "42"
+    doc = json.load(open(js))
+    assert len(doc["rows"]) == 6 and all(not row["skipped"] for row in doc["rows"])
+
+
+def test_bench_grid_contract_errors(cli):
+    code, _, err = run(cli, "bench", "--methods", "bf,kdt", "--reps", "1")
+    assert code == 3 and "not available" in err
+    code, _, err = run(cli, "bench", "--k", "5000", "--reps", "1")
+    assert code == 3 and "exceeds cell size" in err
