@@ -368,6 +368,32 @@ def test_large_k_block_sizes(knn, oracle, k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", ["huge", "tiny", "offset", "query_outside_range"])
+def test_tensor_path_extreme_magnitudes(knn, oracle, case):
+    """The fp16 filter's centre/scale and rounding radii under extreme
+    coordinate magnitudes: results stay exact (certified, or recomputed by the
+    exact kernel when a query overflows fp16 or the bound is too loose)."""
+    rng = np.random.default_rng({"huge": 1, "tiny": 2, "offset": 3, "query_outside_range": 4}[case])
+    m, n, d, k = 6000, 300, 24, 10
+    R = rng.standard_normal((m, d))
+    Q = rng.standard_normal((n, d))
+    if case == "huge":
+        R, Q = R * 1e18, Q * 1e18
+    elif case == "tiny":
+        R, Q = R * 1e-18, Q * 1e-18
+    elif case == "offset":
+        R, Q = R + 1e4, Q + 1e4
+    else:
+        Q = Q * 1e9
+    R = R.astype(np.float32)
+    Q = Q.astype(np.float32)
+    ri, rd = oracle.knn(Q, R, k)
+    t = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    rep = compare(t.index, t.distance, ri, rd, Q, R, oracle=oracle)
+    assert rep.ok, f"{case}: {rep}"
+
+
+@pytest.mark.gpu
 def test_non_finite_detected_on_device(knn, oracle):
     """The host API validates coordinates on the device copy (point_set.hpp:27-31
     text, first offending coordinate in row-major order)."""
