@@ -191,20 +191,8 @@ __device__ __forceinline__ void push_group_off(float gm, float tf, uint32_t& sgp
         : "memory");
 }
 
-// no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~
-// (all lanes read the same addresses -- broadcasts).  Global (read-only path)
-// or shared-memory source.
-__device__ __forceinline__ void add_rnorm(float (&v)[32], const float* rn) {
-    const float4* nr = reinterpret_cast<const float4*>(rn);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const float4 w = __ldg(nr + j);
-        v[4 * j] += w.x;
-        v[4 * j + 1] += w.y;
-        v[4 * j + 2] += w.z;
-        v[4 * j + 3] += w.w;
-    }
-}
+// no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~,
+// from the warp's shared-memory copy of the unit's norms (broadcast reads)
 __device__ __forceinline__ void add_rnorm_smem(float (&v)[32], const float* rn) {
     const float4* nr = reinterpret_cast<const float4*>(rn);
 #pragma unroll
