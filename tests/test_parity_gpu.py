@@ -394,6 +394,38 @@ def test_tensor_path_extreme_magnitudes(knn, oracle, case):
 
 
 @pytest.mark.gpu
+def test_index_search_captures_into_a_cuda_graph(knn, oracle):
+    """An index search on a caller stream (k <= 32: no host round trip) can be
+    captured into a CUDA graph; replays give the eager result bitwise."""
+    import torch
+    n, m, d, k = 2000, 20000, 40, 16
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        Q = torch.from_numpy(oracle.uniform_f32(n, d, 91)).cuda()
+        R = torch.from_numpy(oracle.uniform_f32(m, d, 92)).cuda()
+        od = torch.empty((n, k), device="cuda")
+        oi = torch.empty((n, k), dtype=torch.int64, device="cuda")
+        ix = knn.Index(device_ptr=R.data_ptr(), m=m, d=d)
+        go = lambda: ix.search_device(Q.data_ptr(), n, k, od.data_ptr(), oi.data_ptr(),
+                                      stream=s.cuda_stream)
+        go()
+        s.synchronize()
+        ref_i, ref_d = oi.clone(), od.clone()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            go()
+        od.zero_()
+        oi.zero_()
+        g.replay()
+        s.synchronize()
+    assert (oi == ref_i).all() and (od == ref_d).all()
+    ri, rd = oracle.knn(Q.cpu().numpy()[:200], R.cpu().numpy(), k)
+    assert compare(oi.cpu().numpy()[:200], od.cpu().numpy()[:200], ri, rd,
+                   Q.cpu().numpy()[:200], R.cpu().numpy(), oracle=oracle).ok
+    ix.close()
+
+
+@pytest.mark.gpu
 def test_non_finite_detected_on_device(knn, oracle):
     """The host API validates coordinates on the device copy (point_set.hpp:27-31
     text, first offending coordinate in row-major order)."""
