@@ -426,6 +426,21 @@ def test_index_search_captures_into_a_cuda_graph(knn, oracle):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("metric", [EUCLIDEAN, MANHATTAN])
+def test_full_sort_k_equals_m(knn, oracle, metric):
+    """k = m (the full sort, test_bruteforce.cpp:86-89 at scale): global lists,
+    merge scratch for k > 2048 and the exact path for k > 1024."""
+    m, n, d = 2600, 20, 7
+    R = oracle.uniform_f32(m, d, 801)
+    Q = oracle.uniform_f32(n, d, 802)
+    ri, rd = oracle.knn(Q, R, m, metric)
+    t = knn.bf_knn(Q, R, m, knn.Metric(metric))
+    rep = compare(t.index, t.distance, ri, rd, Q, R, metric, oracle=oracle)
+    assert rep.ok, str(rep)
+    check_invariants(t, m)
+
+
+@pytest.mark.gpu
 def test_non_finite_detected_on_device(knn, oracle):
     """The host API validates coordinates on the device copy (point_set.hpp:27-31
     text, first offending coordinate in row-major order)."""
