@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "exact_kernel.cuh"
 #include "profile.cuh"
+#include "sm100.cuh"
 #include "warp_list.cuh"
 
 namespace knnb200 {
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
 
     // stream-K: this CTA owns units [u, u_end) of the (query block, tile)
     // sequence; each query block it touches is one segment with its own lists
+    sm100::pdl_wait();  // device fallback: the re-rank's query list is complete
     const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
     if (n_eff <= 0) return;
     const ExactSplit sp = exact_split(n_eff, a.ntiles, gridDim.x);
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(MX_WARPS * 32) merge_exact_kernel(ExactArgs a,
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int k = a.k;
+    sm100::pdl_wait();  // the exact kernel's segment slots are complete
     const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
     const ExactSplit sp = exact_split(n_eff, a.ntiles, a.max_ctas);
     for (int64_t q = static_cast<int64_t>(blockIdx.x) * MX_WARPS + warp; q < n_eff;
@@ -405,7 +408,7 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
                                         static_cast<int>(smem)));
     {
         ProfileScope ps(stream, smem_lists ? "exact_knn_kernel" : "exact_knn_kernel_glist");
-        kern<<<a.max_ctas, THREADS, smem, stream>>>(a);
+        KNN_CUDA_CHECK(launch_kernel(kern, a.max_ctas, THREADS, smem, stream, a.qcount != nullptr && pdl_enabled(4), a));
     }
     KNN_LAUNCH_CHECK();
     // merge the blocks spread over several CTAs (host-known counts: only if any)
@@ -429,9 +432,11 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
         KNN_CUDA_CHECK(cudaFuncSetAttribute(merge_exact_kernel<M, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(mx_bytes)));
-        merge_exact_kernel<M, true><<<grid, MX_WARPS * 32, mx_bytes, stream>>>(a, nullptr, nullptr);
+        KNN_CUDA_CHECK(launch_kernel(merge_exact_kernel<M, true>, grid, MX_WARPS * 32, mx_bytes, stream,
+                                     pdl_enabled(4), a, static_cast<float*>(nullptr), static_cast<int64_t*>(nullptr)));
     } else {
-        merge_exact_kernel<M, false><<<grid, MX_WARPS * 32, 0, stream>>>(a, a.mglist_key, a.mglist_idx);
+        KNN_CUDA_CHECK(launch_kernel(merge_exact_kernel<M, false>, grid, MX_WARPS * 32, 0, stream, pdl_enabled(4),
+                                     a, a.mglist_key, a.mglist_idx));
     }
     KNN_LAUNCH_CHECK();
 }

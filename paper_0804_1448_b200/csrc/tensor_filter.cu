@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    sm100::pdl_wait();  // the query prep (the predecessor) is complete from here on
 
     if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
     const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #undef KNN_FLUSH
     }
 
+    sm100::pdl_trigger();
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    sm100::pdl_wait();  // the query prep (the predecessor) is complete from here on
 
     if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
     const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (cur_p >= 0) finish();
     }
 
+    sm100::pdl_trigger();
     sm100::tc_fence_before();
     __syncthreads();
     if (warp == 2) {
@@ -499,7 +503,7 @@ void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const F
         KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         ProfileScope ps(stream, "tc_filter_kernel");
-        kern<<<G, THREADS, smem, stream>>>(tq, tr, fa);
+        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
     };
     switch (Kq) {
         case 4: go(filter_kernel<4>); break;
@@ -520,7 +524,7 @@ void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const Fil
                                         static_cast<int>(smem)));
     {
         ProfileScope ps(stream, "tc_filter_fixed_kernel");
-        filter_fixed_kernel<0><<<G, THREADS, smem, stream>>>(tq, tr, fa);
+        KNN_CUDA_CHECK(launch_kernel(filter_fixed_kernel<0>, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
     }
     KNN_LAUNCH_CHECK();
 }

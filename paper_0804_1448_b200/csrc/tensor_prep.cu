@@ -111,6 +111,7 @@ __global__ void scale_kernel(const unsigned* mn, const unsigned* mx, int d, int 
 // warp per row: fp16 conversion, folded norm, rounding radius
 template <bool QUERY>
 __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
+    if (QUERY) sm100::pdl_trigger();  // the filter may start its prologue
     __shared__ float red[2][8];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;

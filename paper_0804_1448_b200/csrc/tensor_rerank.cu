@@ -25,6 +25,7 @@ namespace {
 // logged values <= tau; their exact FP32 keys (key_step<kL2>, bitwise the
 // exact kernel's arithmetic); (4) exact top-k by (key, index) rank counting.
 __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
+    sm100::pdl_wait();  // the filter's lists and logs are complete
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -232,8 +233,9 @@ __global__ void scatter_rows_kernel(const float* src_d, const int64_t* src_i, co
 void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream) {
     {
         ProfileScope ps(stream, "rerank_kernel");
-        rerank_kernel<<<static_cast<unsigned>((ra.n + RR_WARPS - 1) / RR_WARPS), RR_WARPS * 32, smem,
-                        stream>>>(ra);
+        KNN_CUDA_CHECK(launch_kernel(rerank_kernel,
+                                     static_cast<unsigned>((ra.n + RR_WARPS - 1) / RR_WARPS),
+                                     RR_WARPS * 32, smem, stream, pdl_enabled(2), ra));
     }
     KNN_LAUNCH_CHECK();
 }

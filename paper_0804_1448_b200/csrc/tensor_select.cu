@@ -204,6 +204,7 @@ __device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist
 // capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
 template <int NT>
 __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(LargeArgs a) {  // <= 64 registers
+    sm100::pdl_wait();  // the fixed filter's logs are complete
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
     int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
@@ -330,7 +331,7 @@ void launch_select_large(const LargeArgs& la, cudaStream_t stream) {
                                         static_cast<int>(smem)));
     {
         ProfileScope ps(stream, "select_large_kernel");
-        sel<<<static_cast<unsigned>(la.n), nt, smem, stream>>>(la);
+        KNN_CUDA_CHECK(launch_kernel(sel, static_cast<unsigned>(la.n), nt, smem, stream, pdl_enabled(2), la));
     }
     KNN_LAUNCH_CHECK();
 }
