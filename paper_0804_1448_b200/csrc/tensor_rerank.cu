@@ -77,7 +77,23 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     //    sorted, so an entry's rank is its own position plus, per other list,
     //    a binary search: entries <= v of earlier lists, < v of later ones.
     float B = kInf;
-    if (L >= k) {
+    if (L >= k && nslots <= 2) {
+        // One or two lists (the common stream-K case): lane i tests the split
+        // "i smallest of list 0, k-i of list 1"; every valid split takes a
+        // multiset of the k smallest values, so its maximum is the k-th value.
+        const int cA = __shfl_sync(0xffffffffu, cnt, 0);
+        const int cB = L - cA;
+        const float* sb = sv + cA;
+        for (int i = lane; i <= k; i += 32) {
+            const int j = k - i;
+            if (i <= cA && j <= cB &&
+                (i == 0 || j == cB || sv[i - 1] <= sb[j]) &&
+                (j == 0 || i == cA || sb[j - 1] <= sv[i]))
+                B = fmaxf(i > 0 ? sv[i - 1] : -kInf, j > 0 ? sb[j - 1] : -kInf);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
+    } else if (L >= k) {
         for (int x0 = 0; x0 < L; x0 += 32) {  // warp-uniform trip count (shuffles inside)
             const int x = x0 + lane;
             const bool valid = x < L;
