@@ -57,6 +57,12 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
         nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
+    // the first two lists are read speculatively (entries past cnt unused),
+    // in the same memory round trip as the counts
+    float pa[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+        pa[p] = (p < nslots && lane < Kq) ? a.f.part_A[((p0 + p) * Kq + lane) * TILE + row] : kInf;
     const Consts qc = load_consts(a.f, q);
     // 0. all bound lists, compacted: list p's entries go to [excl_p, excl_p + cnt_p)
     int cincl = cnt;
@@ -69,7 +75,8 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     for (int p = 0; p < nslots; ++p) {  // a list holds <= Kq <= 32 entries
         const int cp = __shfl_sync(0xffffffffu, cnt, p);
         const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
-        if (lane < cp) sv[ep + lane] = a.f.part_A[((p0 + p) * Kq + lane) * TILE + row];
+        if (lane < cp)
+            sv[ep + lane] = p < 2 ? pa[p] : a.f.part_A[((p0 + p) * Kq + lane) * TILE + row];
     }
     __syncwarp();
 
@@ -132,15 +139,46 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     if (ok) {
         int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
         int ng = 0;
-        for (int p = 0; p < nslots; ++p) {
-            const int np = __shfl_sync(0xffffffffu, nlog, p);
-            const int base = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG);
-            for (int t0 = 0; t0 < np; t0 += 32) {
-                const int t = t0 + lane;
-                const bool in = t < np && __int_as_float(a.f.log_h[base + t].x) <= tau;
+        // log heads flattened over the parts (part-major), 8 per lane per
+        // round so that one round trip covers up to 256 logged groups
+        int nincl = nlog;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, nincl, o);
+            if (lane >= o) nincl += y;
+        }
+        const int NT = __shfl_sync(0xffffffffu, nincl, 31);
+        int* pend = reinterpret_cast<int*>(sv);  // part ends; the bound lists are consumed
+        __syncwarp();
+        if (lane < nslots) pend[lane] = nincl;
+        __syncwarp();
+        for (int t0 = 0; t0 < NT; t0 += 256) {
+            float hv[8];
+            int hs[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int t = t0 + e * 32 + lane;
+                hv[e] = kInf;
+                hs[e] = 0;
+                if (t < NT) {
+                    int p = 0, ex = 0;
+                    for (int pp = 0; pp + 1 < nslots; ++pp) {
+                        const int pe = pend[pp];
+                        if (t >= pe) {
+                            p = pp + 1;
+                            ex = pe;
+                        }
+                    }
+                    hs[e] = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG) + (t - ex);
+                    hv[e] = __int_as_float(a.f.log_h[hs[e]].x);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool in = hv[e] <= tau;
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
                 const int pos = ng + __popc(bal & ((1u << lane) - 1u));
-                if (in && pos < RR_CAND) gl[pos] = base + t;
+                if (in && pos < RR_CAND) gl[pos] = hs[e];
                 ng += __popc(bal);
             }
         }
