@@ -52,17 +52,19 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     // part slots written for this pair: one per CTA whose unit range touches it
     const int pair = qt >> 1;
     const int nslots = a.f.pair_slots[pair];
+    // Counts and the first two lists are read speculatively for every part
+    // slot of the tile (in bounds; slots >= nslots and entries past cnt are
+    // stale and masked), in the same memory round trip as nslots.
     int cnt = 0, nlog = 0;
-    if (lane < nslots) {
+    if (lane < parts) {
         cnt = a.f.part_cnt[(p0 + lane) * TILE + row];
         nlog = a.f.log_n[(p0 + lane) * TILE + row];
     }
-    // the first two lists are read speculatively (entries past cnt unused),
-    // in the same memory round trip as the counts
     float pa[2];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
-        pa[p] = (p < nslots && lane < Kq) ? a.f.part_A[((p0 + p) * Kq + lane) * TILE + row] : kInf;
+        pa[p] = (p < parts && lane < Kq) ? a.f.part_A[((p0 + p) * Kq + lane) * TILE + row] : kInf;
+    if (lane >= nslots) cnt = nlog = 0;
     const Consts qc = load_consts(a.f, q);
     // 0. all bound lists, compacted: list p's entries go to [excl_p, excl_p + cnt_p)
     int cincl = cnt;
