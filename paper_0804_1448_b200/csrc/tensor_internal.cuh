@@ -219,6 +219,27 @@ __device__ __forceinline__ void ldg8(const float* p, float (&v)[8]) {
                  : "l"(p));
 }
 
+// 256-bit load with an L2 eviction-priority policy (createpolicy operand)
+__device__ __forceinline__ void ldg8_hint(const float* p, float (&v)[8], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                   "=f"(v[6]), "=f"(v[7])
+                 : "l"(p), "l"(pol));
+}
+
+__device__ __forceinline__ int ldg_hint(const int* p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// read-once data (the group logs): evicted before the reference rows
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 // Exact FP32 key of one (query row, reference row) pair, key_step order.
 // Rows 32-byte aligned (d % 8 == 0, 32-byte aligned bases): 256-bit loads.
 __device__ __forceinline__ float exact_key_l2(const float* qrow, const float* rrow, int d) {

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     int nc = 0;
     if (ok) {
         int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
+        const uint64_t pol = l2_evict_first_policy();  // the logs are read once
         int ng = 0;
         // log heads flattened over the parts (part-major), 8 per lane per
         // round so that one round trip covers up to 256 logged groups
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
                         }
                     }
                     hs[e] = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG) + (t - ex);
-                    hv[e] = __int_as_float(a.f.log_h[hs[e]].x);
+                    hv[e] = __int_as_float(ldg_hint(reinterpret_cast<const int*>(a.f.log_h + hs[e]), pol));
                 }
             }
 #pragma unroll
@@ -194,8 +195,9 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
             for (int e = 0; e < 8; ++e) w[e] = kInf;
             if (j < ng) {
                 const int slot = gl[j];
-                ldg8(reinterpret_cast<const float*>(a.f.log_v + 2 * static_cast<int64_t>(slot)), w);
-                c0 = a.f.log_h[slot].y;
+                ldg8_hint(reinterpret_cast<const float*>(a.f.log_v + 2 * static_cast<int64_t>(slot)), w,
+                          pol);
+                c0 = ldg_hint(reinterpret_cast<const int*>(a.f.log_h + slot) + 1, pol);
             }
             __syncwarp();
 #pragma unroll
