@@ -38,9 +38,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned char* As = base;                // 2 query tiles
     unsigned char* Bs = base + 2 * KBB;      // stages x reference tile
     float* GB = reinterpret_cast<float*>(Bs + a.stages * KBB);        // [CAP][512] group minima
-    uint64_t* sT = reinterpret_cast<uint64_t*>(GB + CAP * EPI_THREADS);  // [2][128] tagged bounds
-    uint64_t* sP = sT + 2 * TILE;                                       // [2][2][128] tagged kp-th
-    float* RN = reinterpret_cast<float*>(sP + 4 * TILE);  // [EPI_WARPS][128] staged ||r~||^2 (no-fold)
+    float* RN = GB + CAP * EPI_THREADS;  // [EPI_WARPS][128] staged ||r~||^2 (no-fold)
     uint64_t* bars = reinterpret_cast<uint64_t*>(RN + EPI_WARPS * TILE);
     uint64_t* full = bars;
     uint64_t* empty = bars + a.stages;
@@ -50,7 +48,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tempty = tfull + 4;  // [query tile][parity]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
-    const int warp = threadIdx.x >> 5;
+    // warp index via a shuffle: ptxas then knows it is warp-uniform and keeps
+    // role-branch state (e.g. the global memory descriptor) in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
     const int64_t u_begin = unit_start(a.U, a.G, cta);
@@ -69,7 +69,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         sm100::fence_mbar_init();
     }
-    for (int i = threadIdx.x; i < 6 * TILE; i += blockDim.x) sT[i] = ~0ull;  // no tag matches
     if (warp == 2) sm100::tmem_alloc(tmem_slot, 512);
     sm100::tc_fence_before();
     __syncthreads();
@@ -100,73 +99,70 @@ __global__ void __launch_bounds__(THREADS, 1)
         L.reset();
         int cur_p = -1;
         uint32_t sgp = sg0;  // next buffer slot: (sgp - sg0) / (4 EPI_THREADS) minima buffered
-        float T = kInf;    // own bound: thresh(k-th smallest group minimum of this list)
-        float Tf = kInf;   // filter bound: min over every valid bound for this query
+        float T = kInf;      // own bound: thresh(k-th smallest group minimum of this list)
+        float Tf = kInf;     // filter bound: min over every valid bound for this query
+        float tfp = kInf;    // push bound: Tf, or -inf once the log is (nearly) full
         unsigned tg_pref = 0xffffffffu;  // prefetched cross-CTA bound (ordered uint)
         Consts qc{};
-        int64_t q = 0;
-        int64_t part = 0;
-        const float4* lvb = nullptr;  // this (query, part)'s group log
-        const int2* lhb = nullptr;
-        int ln = 0;            // groups logged so far (may exceed CG: overflow)
-        unsigned long long st_drains = 0, st_rounds = 0;
-        long long st_cyc_drain = 0, st_cyc_wait = 0;
-        const long long st_cyc0 = kStats ? clock64() : 0;
+        int q = 0;
+        int part = 0;
+        float4* lvb = nullptr;  // this (query, part)'s group log: values, heads
+        int2* lhb = nullptr;
+        int ln = 0;             // groups logged so far
 
         // Drain: one buffered group minimum per lane per round into the bound
-        // list, then refresh the bound from (1) this list, (2) the other
-        // parity's list of the same query (smem, tagged by pair), (3) the union
-        // of both lists' ceil(k/2)-th values, (4) other CTAs' lists (global
-        // atomicMin, read one drain late so the load latency hides).
+        // list, then refresh the bound from this list and other CTAs' lists
+        // (global atomicMin, read one drain late so the load latency hides).
 #define KNN_DRAIN()                                                                              \
     do {                                                                                         \
-        const long long c0_ = (kStats && a.stats) ? clock64() : 0;                                           \
-        if (kStats && a.stats) ++st_drains;                                                                \
         const int nb = static_cast<int>((sgp - sg0) / (EPI_THREADS * 4));                       \
         const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
         _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
-            if (kStats && a.stats) ++st_rounds;                                                            \
             const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
             /* a minimum at or above the list's last entry changes nothing */                  \
             if (__any_sync(0xffffffffu, g_ <= Tf && g_ < L.key[KR - 1])) L.insert(g_);           \
         }                                                                                        \
         sgp = sg0;                                                                               \
-        if (L.cnt >= k) T = fminf(T, thresh(L.kth(k), qc));                                      \
-        float tf_ = fminf(T, dec_or_inf(tg_pref));                                               \
-        if (T < kInf) atomicMin(a.tglob + q, enc(T));                                            \
+        if (L.cnt >= k) {                                                                        \
+            const float tn_ = thresh(L.kth(k), qc);                                              \
+            if (tn_ < T) {                                                                       \
+                T = tn_;                                                                         \
+                atomicMin(a.tglob + q, enc(T));                                                  \
+            }                                                                                    \
+        }                                                                                        \
+        Tf = fminf(T, dec_or_inf(tg_pref));                                                      \
         tg_pref = __ldcg(a.tglob + q);                                                           \
-        Tf = tf_;                                                                                \
-        if (kStats && a.stats) st_cyc_drain += clock64() - c0_;                                            \
     } while (0)
 
 #define KNN_FLUSH()                                                                              \
     do {                                                                                         \
-        float* pa_ = a.part_A + part * a.Kq * TILE;                                              \
+        float* pa_ = a.part_A + static_cast<int64_t>(part) * a.Kq * TILE;                        \
         _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_)                                        \
             if (e_ < L.cnt) pa_[e_ * TILE + row] = L.key[e_];                                    \
         a.part_cnt[part * TILE + row] = L.cnt;                                                   \
-        a.log_n[part * TILE + row] = ln;                                                         \
+        a.log_n[part * TILE + row] = ln > a.CG - 16 ? a.CG + 1 : ln; /* (nearly) full: overflow */ \
     } while (0)
 
-        // One 32-column chunk, branch-free: the minimum of each 8-column group
-        // (FMNMX3); every group whose minimum is under the lane's bound is
-        // pushed (predicated stores): its minimum to the smem buffer, its 8
-        // values to the global log.  With 32 queries per warp some lane hits
-        // in most chunks, so a hit must not cost a divergent branch.
-#define KNN_SCAN_CHUNK(vv, colb)                                                                 \
+        // One 32-column chunk, branch-free: the FMNMX3 minimum of each 8-column
+        // group; if some lane of the warp has a group under its bound, all four
+        // groups are pushed with predicated stores (a hit must not cost a
+        // divergent branch: with 32 queries per warp most chunks hit).
+#define KNN_SCAN32(rr, colb)                                                                     \
     do {                                                                                         \
+        float v_[32];                                                                            \
+        _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
+        if (!a.fold) add_rnorm_smem(v_, rnw + ((colb) - col_base));                              \
         float gm_[4];                                                                            \
-        bool any_ = false;                                                                       \
         _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                       \
-            const float* w_ = vv + 8 * i_;                                                       \
+            const float* w_ = v_ + 8 * i_;                                                       \
             gm_[i_] = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]), w_[6]),   \
                             w_[7]);                                                              \
-            any_ |= gm_[i_] <= Tf;                                                               \
         }                                                                                        \
-        if (a.mode != 3 && __any_sync(0xffffffffu, any_)) { /* some lane pushes: most chunks */ \
+        if (a.mode != 3 &&                                                                       \
+            __any_sync(0xffffffffu, fminf(fminf(gm_[0], gm_[1]), fminf(gm_[2], gm_[3])) <= tfp)) { \
             _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_)                                     \
-                push_group_off<EPI_THREADS * 4>(gm_[i_], Tf, sgp, ln, a.CG, lvb, lhb, vv + 8 * i_, \
-                                                (colb) + 8 * i_);                                \
+                push_group<EPI_THREADS * 4>(gm_[i_], tfp, sgp, ln, lvb, lhb, v_ + 8 * i_,        \
+                                            (colb) + 8 * i_);                                    \
         }                                                                                        \
     } while (0)
 
@@ -176,9 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t tlane = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
                                static_cast<uint32_t>(2 * grp * TILE);
         auto wait_full = [&](int t) {
-            const long long cw_ = (kStats && a.stats) ? clock64() : 0;
             sm100::mbar_wait(tfull + 2 * grp + (t & 1), static_cast<uint32_t>((t >> 1) & 1));
-            if (kStats && a.stats) st_cyc_wait += clock64() - cw_;
             sm100::tc_fence_after();
         };
         auto release = [&](int t) {
@@ -203,13 +197,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4 rn_nx = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!a.fold && nunits > 0)
             rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + rt * TILE) + lane);
-#define KNN_SCAN_REGS(rr, colb)                                                                  \
-    do {                                                                                         \
-        float v_[32];                                                                            \
-        _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
-        if (!a.fold) add_rnorm_smem(v_, rnw + ((colb) - col_base));                              \
-        KNN_SCAN_CHUNK(v_, colb);                                                                \
-    } while (0)
         for (int t = 0; t < nunits; ++t) {
             if (p != cur_p) {
                 if (cur_p >= 0) {
@@ -218,10 +205,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 cur_p = p;
                 const int qt = 2 * p + grp;
-                q = static_cast<int64_t>(qt) * TILE + row;
+                q = qt * TILE + row;
                 const int slot = cta - first_cta_of(static_cast<int64_t>(p) * a.rtiles, a.U, a.G);
-                part = static_cast<int64_t>(qt) * a.S_max + slot;
-                const int64_t lq = (part * TILE + row) * a.CG;
+                part = qt * a.S_max + slot;
+                const int64_t lq = (static_cast<int64_t>(part) * TILE + row) * a.CG;
                 lvb = a.log_v + 2 * lq;
                 lhb = a.log_h + lq;
                 ln = 0;
@@ -232,6 +219,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 Tf = dec_or_inf(tg_pref);
                 sgp = sg0;
             }
+            // a unit pushes <= 16 groups: stop pushing (the query then fails the
+            // certificate and is recomputed exactly) once fewer slots are left
+            tfp = ln > a.CG - 16 ? -kInf : Tf;
             const int col_base = rt * TILE;
             const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
             if (!a.fold) {  // stage this unit's norms, prefetch the next unit's
@@ -248,16 +238,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 release(t);
             } else {
                 sm100::tmem_ld_32x32b_x32(taddr + 32, rb);
-                KNN_SCAN_REGS(ra, col_base);
+                KNN_SCAN32(ra, col_base);
                 sm100::tmem_ld_wait();
                 sm100::tmem_ld_32x32b_x32(taddr + 64, ra);
-                KNN_SCAN_REGS(rb, col_base + 32);
+                KNN_SCAN32(rb, col_base + 32);
                 sm100::tmem_ld_wait();
                 sm100::tmem_ld_32x32b_x32(taddr + 96, rb);
-                KNN_SCAN_REGS(ra, col_base + 64);
+                KNN_SCAN32(ra, col_base + 64);
                 sm100::tmem_ld_wait();
                 release(t);  // all four chunks of tile t are in registers
-                KNN_SCAN_REGS(rb, col_base + 96);
+                KNN_SCAN32(rb, col_base + 96);
                 // drain after the release, so the MMA never waits on the list
                 if (__any_sync(0xffffffffu, sgp - sg0 >= static_cast<uint32_t>(a.drain_at * EPI_THREADS * 4)))
                     KNN_DRAIN();
@@ -272,25 +262,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ++p;
             }
         }
-#undef KNN_SCAN_REGS
         if (cur_p >= 0) {
             KNN_DRAIN();
             KNN_FLUSH();
         }
-        if (kStats && a.stats) {
-            const unsigned long long lg = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(ln));
-            if (lane == 0) {
-                atomicAdd(a.stats + 0, lg);
-                atomicAdd(a.stats + 1, st_drains);
-                atomicAdd(a.stats + 2, st_rounds);
-                atomicAdd(a.stats + 3, lg);
-                atomicAdd(a.stats + 4, static_cast<unsigned long long>(nunits));
-                atomicAdd(a.stats + 5, static_cast<unsigned long long>(st_cyc_drain));
-                atomicAdd(a.stats + 6, static_cast<unsigned long long>(st_cyc_wait));
-                atomicAdd(a.stats + 7, static_cast<unsigned long long>(clock64() - st_cyc0));
-            }
-        }
-#undef KNN_SCAN_CHUNK
+#undef KNN_SCAN32
 #undef KNN_DRAIN
 #undef KNN_FLUSH
     }
@@ -331,7 +307,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tempty = tfull + 4;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
 
-    const int warp = threadIdx.x >> 5;
+    // warp index via a shuffle: ptxas then knows it is warp-uniform and keeps
+    // role-branch state (e.g. the global memory descriptor) in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
     const int64_t u_begin = unit_start(a.U, a.G, cta);

@@ -119,6 +119,7 @@ struct FilterArgs {
     int CG;                // log capacity (groups) per (part, query)
     int drain_at;          // drain when a lane holds this many group minima (<= CAP - 16)
     int mode;              // dev only (KNN_B200_FILTER_MODE): 0 full, 2 no epilogue work, 3 no pushes
+    int dev_flags;         // dev only (KNN_B200_DEV_FLAGS): bit 0 MMA issuers spin instead of sleeping
     float* sink;
     unsigned long long* stats;  // dev only (KNN_B200_FILTER_STATS)
     // large-k (filter_fixed_kernel): seed tiles per segment, per-query
@@ -161,34 +162,35 @@ constexpr bool kStats = true;
 constexpr bool kStats = false;
 #endif
 
-constexpr int CAP = 32;        // per-lane buffered group minima awaiting the bound list (smem);
+constexpr int CAP = 24;        // per-lane buffered group minima awaiting the bound list (smem);
                                // drained once per tile (a tile pushes <= 16), off the TMEM path
 constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow by what warpgroup 0 frees
 // (the pool is the CTA's launch allocation: 2 x 128 x (232 - 168) = 128 x (168 - 40))
 constexpr int CTRL_REGS = 40;
 
-// push_group with the bookkeeping folded into the predicates: `off` counts the
-// groups logged by this (query, part) including overflow (slot = off), `sgp`
-// is the next smem buffer slot; both advance only on a hit.
+// Push of one 8-column group whose minimum is under the lane's bound: its 8
+// values (32 B) and head {minimum, first column} at slot `off` of the query's
+// log, the minimum into the lane's smem buffer (for the drain).  The stores
+// are predicated in PTX (never a branch); the cursor updates stay in C++ so
+// ptxas sees plain selects.  Capacity is checked once per unit by the caller.
 template <int STRIDE>
-__device__ __forceinline__ void push_group_off(float gm, float tf, uint32_t& sgp, int& off, int cg,
-                                               const float4* lvb, const int2* lhb, const float* w,
-                                               int col) {
+__device__ __forceinline__ void push_group(float gm, float tf, uint32_t& sgp, int& off, float4* lvb,
+                                           int2* lhb, const float* w, int col) {
+    const bool hit = gm <= tf;
+    float4* pv = lvb + 2 * off;
+    int2* ph = lhb + off;
     asm volatile(
-        "{\n\t.reg .pred p, q;\n\t.reg .u64 a, b;\n\t"
-        "setp.le.f32 p, %2, %3;\n\t"
-        "setp.lt.and.s32 q, %1, %4, p;\n\t"
-        "@p st.shared.f32 [%0], %2;\n\t"
-        "mad.wide.s32 a, %1, 32, %5;\n\t"
-        "mad.wide.s32 b, %1, 8, %6;\n\t"
-        "@q st.global.v8.f32 [a], {%8, %9, %10, %11, %12, %13, %14, %15};\n\t"
-        "@q st.global.v2.b32 [b], {%2, %7};\n\t"
-        "@p add.s32 %1, %1, 1;\n\t"
-        "@p add.s32 %0, %0, %16;\n\t}"
-        : "+r"(sgp), "+r"(off)
-        : "f"(gm), "f"(tf), "r"(cg), "l"(lvb), "l"(lhb), "r"(col), "f"(w[0]), "f"(w[1]), "f"(w[2]),
-          "f"(w[3]), "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "n"(STRIDE)
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %0, 0;\n\t"
+        "@p st.global.v8.f32 [%1], {%5, %6, %7, %8, %9, %10, %11, %12};\n\t"
+        "@p st.global.v2.b32 [%2], {%3, %4};\n\t"
+        "@p st.shared.f32 [%13], %3;\n\t}"
+        :
+        : "r"(static_cast<int>(hit)), "l"(pv), "l"(ph), "f"(gm), "r"(col), "f"(w[0]), "f"(w[1]),
+          "f"(w[2]), "f"(w[3]), "f"(w[4]), "f"(w[5]), "f"(w[6]), "f"(w[7]), "r"(sgp)
         : "memory");
+    off += hit ? 1 : 0;
+    sgp += hit ? STRIDE : 0;
 }
 
 // no-fold layouts: add ||r~||^2 of 32 consecutive references to the raw -2 q~.r~,
@@ -390,6 +392,13 @@ __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUten
     }
 }
 
+// The MMA issuers wait with a suspend-time hint: a spinning issuer would take
+// issue slots from the two epilogue warps sharing its SM sub-partition.
+__device__ __forceinline__ void mma_wait(const FilterArgs& a, uint64_t* bar, uint32_t parity) {
+    if (a.dev_flags & 1) sm100::mbar_wait(bar, parity);
+    else sm100::mbar_wait_sleep(bar, parity);
+}
+
 // One elected thread per query tile g (warps 1 and 3): per unit an M=128
 // N=128 MMA chain into TMEM buffer [g][unit parity].  Two issuers, so a slow
 // epilogue group of one query tile never holds back the other tile's MMAs;
@@ -406,17 +415,17 @@ __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int
     for (; sq.more(); sq.next(), ++t) {
         if (sq.p != cur_p) {
             if (cur_p >= 0) sm100::mma_commit(P.a_empty);
-            sm100::mbar_wait(P.a_full, a_par);
+            mma_wait(a, P.a_full, a_par);
             a_par ^= 1u;
             cur_p = sq.p;
         }
         const int b = static_cast<int>(t & 1);
         const uint32_t tpar = static_cast<uint32_t>((t >> 1) & 1);
-        sm100::mbar_wait(P.full + stage, phase);
+        mma_wait(a, P.full + stage, phase);
         sm100::tc_fence_after();
         const uint32_t b0 = sm100::smem_u32(P.Bs + stage * P.KBB);
         {
-            sm100::mbar_wait(P.tempty + 2 * g + b, tpar ^ 1u);
+            mma_wait(a, P.tempty + 2 * g + b, tpar ^ 1u);
             sm100::tc_fence_after();
             const uint32_t a0 = sm100::smem_u32(P.As + g * P.KBB);
             const uint32_t dt = P.tmem + static_cast<uint32_t>((2 * g + b) * TILE);
@@ -503,8 +512,9 @@ inline Layout layout_for(int d, int k) {
         ncol = L.d16;
     }
     const int kb_fold = (kfold + 63) / 64;
-    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 + 6 * TILE * 8 +
-                       static_cast<size_t>(EPI_WARPS) * TILE * 4;  // + staged reference norms
+    // epilogue smem: group-minimum buffers + staged reference norms (no-fold)
+    const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 +
+                       static_cast<size_t>(EPI_WARPS) * TILE * 4;
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
     auto stages_for = [&](int KB) {
         const size_t per = static_cast<size_t>(KB) * 16384;

@@ -124,6 +124,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     const int64_t n_pad = static_cast<int64_t>(qtiles) * TILE;
     const int64_t m_pad = static_cast<int64_t>(rtiles) * TILE;
     const int64_t U = static_cast<int64_t>(pairs) * rtiles;
+    const bool large = k > MAX_KQ;
     // at most ~29 CTAs share a query-tile pair, so a query has <= 32 partial lists
     const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
                                                      static_cast<int64_t>(pairs) * 29));
@@ -140,7 +141,6 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     Sizer sz;
     sz.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
     sz.take<float4>(static_cast<size_t>(n_pad));
-    const bool large = k > MAX_KQ;
     // group-log capacity: ~1.5x the expected number of running-bound records
     // of a whole pair stream, k (1 + ln(groups / k)), at least 256
     int CG = 0;
@@ -248,6 +248,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     fa.pair_slots = pair_slots;
     fa.CG = CG;
     if (const char* e = std::getenv("KNN_B200_FILTER_MODE")) fa.mode = std::atoi(e);
+    if (const char* e = std::getenv("KNN_B200_DEV_FLAGS")) fa.dev_flags = std::atoi(e);
     fa.drain_at = 8;
     if (const char* e = std::getenv("KNN_B200_DRAIN_AT"))
         fa.drain_at = std::max(1, std::min(CAP - 16, std::atoi(e)));

@@ -138,8 +138,12 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     //    every part (flattened over parts), then the values of the groups whose
     //    minimum is inside tau, then their values <= tau.
     int nc = 0;
+    auto head_of = [&](int64_t slot) { return reinterpret_cast<const int*>(a.f.log_h + slot); };
+    auto log_slot = [&](int h) -> int64_t {
+        return ((p0 + (h >> 16)) * TILE + row) * static_cast<int64_t>(a.f.CG) + (h & 0xffff);
+    };
     if (ok) {
-        int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (log slot), reuses ck
+        int* gl = reinterpret_cast<int*>(ck);  // in-tau groups (part-relative handles), reuses ck
         const uint64_t pol = l2_evict_first_policy();  // the logs are read once
         int ng = 0;
         // log heads flattened over the parts (part-major), 8 per lane per
@@ -172,8 +176,10 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
                             ex = pe;
                         }
                     }
-                    hs[e] = static_cast<int>(((p0 + p) * TILE + row) * a.f.CG) + (t - ex);
-                    hv[e] = __int_as_float(ldg_hint(reinterpret_cast<const int*>(a.f.log_h + hs[e]), pol));
+                    // part-relative handle (part << 16 | slot, CG <= 4096): the global
+                    // slot needs 64 bits once parts * 128 * CG >= 2^31
+                    hs[e] = (p << 16) | (t - ex);
+                    hv[e] = __int_as_float(ldg_hint(head_of(log_slot(hs[e])), pol));
                 }
             }
 #pragma unroll
@@ -194,10 +200,9 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) w[e] = kInf;
             if (j < ng) {
-                const int slot = gl[j];
-                ldg8_hint(reinterpret_cast<const float*>(a.f.log_v + 2 * static_cast<int64_t>(slot)), w,
-                          pol);
-                c0 = ldg_hint(reinterpret_cast<const int*>(a.f.log_h + slot) + 1, pol);
+                const int64_t slot = log_slot(gl[j]);
+                ldg8_hint(reinterpret_cast<const float*>(a.f.log_v + 2 * slot), w, pol);
+                c0 = ldg_hint(head_of(slot) + 1, pol);
             }
             __syncwarp();
 #pragma unroll
