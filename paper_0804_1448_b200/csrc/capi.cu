@@ -101,6 +101,28 @@ void throw_non_finite(unsigned long long i, int64_t d) {
                           std::to_string(static_cast<int64_t>(i) % d));
 }
 
+}  // namespace
+
+// Device-input value check (point_set.hpp:27-31) for the synchronous device
+// APIs: first non-finite coordinate, with the reference's message.
+void check_finite_device(cudaStream_t s, const float* X, int64_t rows, int64_t d,
+                         unsigned long long* dbad) {
+    const int64_t count = rows * d;
+    unsigned long long* tmp = dbad;
+    if (!tmp) KNN_CUDA_CHECK(cudaMallocAsync(&tmp, sizeof(unsigned long long), s));
+    KNN_CUDA_CHECK(cudaMemsetAsync(tmp, 0xff, sizeof(unsigned long long), s));
+    finite_scan_kernel<<<static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, s>>>(
+        X, count, tmp);
+    KNN_LAUNCH_CHECK();
+    unsigned long long bad = 0;
+    KNN_CUDA_CHECK(cudaMemcpyAsync(&bad, tmp, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    if (!dbad) KNN_CUDA_CHECK(cudaFreeAsync(tmp, s));
+    KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (bad != ~0ull) throw_non_finite(bad, d);
+}
+
+namespace {
+
 // Metric::mahalanobis (metric.cpp:20-61): validate, Cholesky M = L L^T.
 std::vector<double> cholesky_or_throw(const double* M, int64_t d) {
     if (d <= 0) throw InvalidArgument("Metric: Mahalanobis dimension must be >= 1");
@@ -227,9 +249,9 @@ struct knn_b200_index {
     int d = 0;
     int64_t base = 0;
     std::mutex mu;
-    // tensor path: the reference set prepared once (fp16 copy, norms, radii)
-    // on the first tensor search, reused by every later search (the KdTree
-    // build/search split, kdtree.hpp:21,70-72)
+    // tensor path: the reference set prepared once, when the index is created
+    // (fp16 copy, norms, radii), reused by every search on any stream (the
+    // KdTree build/search split, kdtree.hpp:21,70-72)
     knnb200::TensorRefs tref;
     void* tref_mem = nullptr;
     ~knn_b200_index() {
@@ -240,14 +262,18 @@ struct knn_b200_index {
 
 namespace knnb200 {
 namespace {
-const TensorRefs* index_refs(knn_b200_index* h, int64_t n, int k, int metric, int path,
-                             cudaStream_t s) {
-    if (plan_search(n, h->m, h->d, k, metric, path).path != 2) return nullptr;
-    if (!h->tref_mem) {
-        KNN_CUDA_CHECK(cudaMalloc(&h->tref_mem, tensor_refs_bytes(h->m, h->d)));
-        tensor_prep_refs(s, h->dR, h->m, h->d, h->tref_mem, h->tref);
-    }
+const TensorRefs* index_refs(knn_b200_index* h, int64_t n, int k, int metric, int path) {
+    if (plan_search(n, h->m, h->d, k, metric, path).path != 2 || !h->tref_mem) return nullptr;
     return &h->tref;
+}
+
+// Eager tensor-path preparation of an index's reference set (d <= 128), on
+// the engine stream and synchronized: searches on any stream may use it.
+void prepare_index(DeviceContext& ctx, knn_b200_index* h) {
+    if (!tensor_path_supported(1, h->m, h->d, 1)) return;
+    KNN_CUDA_CHECK(cudaMalloc(&h->tref_mem, tensor_refs_bytes(h->m, h->d)));
+    tensor_prep_refs(ctx.stream, h->dR, h->m, h->d, h->tref_mem, h->tref);
+    KNN_CUDA_CHECK(cudaStreamSynchronize(ctx.stream));
 }
 }  // namespace
 }  // namespace knnb200
@@ -283,8 +309,8 @@ void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r
     sz.take<int64_t>(static_cast<size_t>(n) * k);
     sz.take<unsigned long long>(2);
     if (chol) sz.take<double>(static_cast<size_t>(dq) * dq);
-    ctx.io.reserve(sz.used + 256);
-    Carver cv{static_cast<char*>(ctx.io.base())};
+    ctx.s->io.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.s->io.base())};
     float* dQ = cv.take<float>(static_cast<size_t>(n) * dq);
     float* dR = cv.take<float>(static_cast<size_t>(m) * dr);
     float* dO = cv.take<float>(static_cast<size_t>(n) * k);
@@ -330,15 +356,20 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     sz.take<int64_t>(static_cast<size_t>(n) * k);
     sz.take<unsigned long long>(2);
     sz.take<int>(static_cast<size_t>(n) + 1);
-    ctx.io.reserve(sz.used + 256);
-    ctx.refs.reserve(tensor_refs_bytes(m, d));
-    Carver cv{static_cast<char*>(ctx.io.base())};
+    const size_t fb_part = k <= 32 ? fallback_part_elems(n, m, k) : 0;
+    sz.take<float>(fb_part);
+    sz.take<int64_t>(fb_part);
+    ctx.s->io.reserve(sz.used + 256);
+    ctx.s->refs.reserve(tensor_refs_bytes(m, d));
+    Carver cv{static_cast<char*>(ctx.s->io.base())};
     float* dQ = cv.take<float>(static_cast<size_t>(n) * d);
     float* dR = cv.take<float>(static_cast<size_t>(m) * d);
     float* dO = cv.take<float>(static_cast<size_t>(n) * k);
     int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
     unsigned long long* dbad = cv.take<unsigned long long>(2);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
+    float* fb_pk = cv.take<float>(fb_part);
+    int64_t* fb_pi = cv.take<int64_t>(fb_part);
     KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), s));
     // every H2D goes through the copy stream in order (R, then the query
@@ -351,7 +382,7 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     finite_scan_kernel<<<scan_grid(m * d), 256, 0, s>>>(dR, m * d, dbad + 1);
     KNN_LAUNCH_CHECK();
     TensorRefs refs;
-    tensor_prep_refs(s, dR, m, d, ctx.refs.base(), refs);
+    tensor_prep_refs(s, dR, m, d, ctx.s->refs.base(), refs);
     // chunks of <= pipe_chunk() queries, at least two (n >= pipe_chunk() here),
     // multiples of the 256-query tile pair
     const int64_t chunks = std::max<int64_t>(2, (n + pipe_chunk() - 1) / pipe_chunk());
@@ -388,6 +419,9 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
         KNN_CUDA_CHECK(cudaMemcpyAsync(out_idx + q0 * k, dI + q0 * k, sizeof(int64_t) * nq * k,
                                        cudaMemcpyDeviceToHost, cs));
     }
+    // uncertified queries of all chunks, resolved once over the whole query
+    // set (small k on the device: exact kernel over the recorded list)
+    tensor_resolve_fallbacks(ctx, s, refs, dQ, n, k, raw_keys, 0, dO, dI, fb, fb_pk, fb_pi);
     unsigned long long bad[2];
     int fails = 0;
     KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));
@@ -396,39 +430,14 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     KNN_CUDA_CHECK(cudaStreamSynchronize(cs));
     if (bad[0] != ~0ull) throw_non_finite(bad[0], d);
     if (bad[1] != ~0ull) throw_non_finite(bad[1], d);
-    ctx.last_fallbacks = fails;
-    ctx.fb_on_device = false;
+    if (!ctx.s->fb_on_device) fails = ctx.s->last_fallbacks;
+    ctx.s->last_fallbacks = fails;
+    ctx.s->fb_on_device = false;
     if (fails == 0) return;
-    // uncertified queries: the full dispatch (large-k retry, exact) on their rows
-    std::vector<int> list(static_cast<size_t>(fails));
-    KNN_CUDA_CHECK(cudaMemcpy(list.data(), fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToHost));
-    std::vector<float> gq(static_cast<size_t>(fails) * d);
-    for (int i = 0; i < fails; ++i)
-        std::memcpy(gq.data() + static_cast<size_t>(i) * d, q + static_cast<int64_t>(list[i]) * d,
-                    sizeof(float) * d);
-    std::vector<float> sd(static_cast<size_t>(fails) * k);
-    std::vector<int64_t> si(static_cast<size_t>(fails) * k);
-    float* gdq = nullptr;
-    float* gdo = nullptr;
-    int64_t* gdi = nullptr;
-    KNN_CUDA_CHECK(cudaMalloc(&gdq, sizeof(float) * gq.size()));
-    KNN_CUDA_CHECK(cudaMalloc(&gdo, sizeof(float) * sd.size()));
-    KNN_CUDA_CHECK(cudaMalloc(&gdi, sizeof(int64_t) * si.size()));
-    KNN_CUDA_CHECK(cudaMemcpy(gdq, gq.data(), sizeof(float) * gq.size(), cudaMemcpyHostToDevice));
-    search_device(ctx, s, gdq, fails, dR, m, d, k, kL2, 2, raw_keys, 0, gdo, gdi);
+    // the chunk results already copied back predate the fallback: copy again
+    KNN_CUDA_CHECK(cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(out_idx, dI, sizeof(int64_t) * n * k, cudaMemcpyDeviceToHost, s));
     KNN_CUDA_CHECK(cudaStreamSynchronize(s));
-    KNN_CUDA_CHECK(cudaMemcpy(sd.data(), gdo, sizeof(float) * sd.size(), cudaMemcpyDeviceToHost));
-    KNN_CUDA_CHECK(cudaMemcpy(si.data(), gdi, sizeof(int64_t) * si.size(), cudaMemcpyDeviceToHost));
-    cudaFree(gdq);
-    cudaFree(gdo);
-    cudaFree(gdi);
-    for (int i = 0; i < fails; ++i) {
-        std::memcpy(out_dist + static_cast<int64_t>(list[i]) * k, sd.data() + static_cast<size_t>(i) * k,
-                    sizeof(float) * k);
-        std::memcpy(out_idx + static_cast<int64_t>(list[i]) * k, si.data() + static_cast<size_t>(i) * k,
-                    sizeof(int64_t) * k);
-    }
-    ctx.last_fallbacks = fails;
 }
 
 }  // namespace
@@ -495,6 +504,7 @@ knn_b200_status knn_b200_search(const float* queries, int64_t n, int32_t dq,
         DeviceContext& ctx = context_for(o.device);
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        ctx.bind(ctx.stream);
         if (plan_search(n, m, dq, k, kernel_metric, o.path).path == 2 && !host_values &&
             n >= pipe_chunk())
             search_pipelined(ctx, q, n, r, m, dq, k, o.raw_keys, out_dist, out_idx);
@@ -526,6 +536,11 @@ knn_b200_status knn_b200_search_device(const float* d_queries, int64_t n,
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        ctx.bind(s);
+        if (!o.stream) {  // synchronous call: validate the values like PointSet does
+            check_finite_device(s, d_queries, n, d, nullptr);
+            check_finite_device(s, d_references, m, d, nullptr);
+        }
         const float* q = d_queries;
         const float* r = d_references;
         int kernel_metric = metric;
@@ -534,8 +549,8 @@ knn_b200_status knn_b200_search_device(const float* d_queries, int64_t n,
             sz.take<float>(static_cast<size_t>(n) * d);
             sz.take<float>(static_cast<size_t>(m) * d);
             sz.take<double>(static_cast<size_t>(d) * d);
-            ctx.io.reserve(sz.used + 256);
-            Carver cv{static_cast<char*>(ctx.io.base())};
+            ctx.s->io.reserve(sz.used + 256);
+            Carver cv{static_cast<char*>(ctx.s->io.base())};
             float* wq = cv.take<float>(static_cast<size_t>(n) * d);
             float* wr = cv.take<float>(static_cast<size_t>(m) * d);
             double* dLT = cv.take<double>(static_cast<size_t>(d) * d);
@@ -580,6 +595,13 @@ knn_b200_status knn_b200_index_create(const float* references, int64_t m, int32_
             delete h;
             KNN_CUDA_CHECK(e);
         }
+        try {
+            std::lock_guard<std::mutex> lock(ctx.mu);
+            prepare_index(ctx, h);
+        } catch (...) {
+            delete h;
+            throw;
+        }
         *out = h;
     });
 }
@@ -593,6 +615,9 @@ knn_b200_status knn_b200_index_create_device(const float* d_references, int64_t 
         if (!out) throw InvalidArgument("knn_b200_index_create: null out");
         check_point_set(d_references, m, d, false);
         DeviceContext& ctx = context_for(o.device);
+        KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        check_finite_device(ctx.stream, d_references, m, d, nullptr);
         auto* h = new knn_b200_index();
         h->device = ctx.device;
         h->dR = d_references;
@@ -600,6 +625,12 @@ knn_b200_status knn_b200_index_create_device(const float* d_references, int64_t 
         h->m = m;
         h->d = d;
         h->base = index_base;
+        try {
+            prepare_index(ctx, h);
+        } catch (...) {
+            delete h;
+            throw;
+        }
         *out = h;
     });
 }
@@ -620,20 +651,20 @@ knn_b200_status knn_b200_index_search(knn_b200_index* index, const float* querie
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        ctx.bind(s);
         Sizer sz;
         sz.take<float>(static_cast<size_t>(n) * index->d);
         sz.take<float>(static_cast<size_t>(n) * k);
         sz.take<int64_t>(static_cast<size_t>(n) * k);
-        ctx.io.reserve(sz.used + 256);
-        Carver cv{static_cast<char*>(ctx.io.base())};
+        ctx.s->io.reserve(sz.used + 256);
+        Carver cv{static_cast<char*>(ctx.s->io.base())};
         float* dQ = cv.take<float>(static_cast<size_t>(n) * index->d);
         float* dO = cv.take<float>(static_cast<size_t>(n) * k);
         int64_t* dI = cv.take<int64_t>(static_cast<size_t>(n) * k);
         KNN_CUDA_CHECK(cudaMemcpyAsync(dQ, queries, sizeof(float) * n * index->d,
                                        cudaMemcpyHostToDevice, s));
         search_device(ctx, s, dQ, n, index->dR, index->m, index->d, k, metric, o.path,
-                      o.raw_keys, index->base, dO, dI,
-                      index_refs(index, n, k, metric, o.path, s));
+                      o.raw_keys, index->base, dO, dI, index_refs(index, n, k, metric, o.path));
         KNN_CUDA_CHECK(
             cudaMemcpyAsync(out_dist, dO, sizeof(float) * n * k, cudaMemcpyDeviceToHost, s));
         KNN_CUDA_CHECK(
@@ -659,9 +690,11 @@ knn_b200_status knn_b200_index_search_device(knn_b200_index* index, const float*
         std::lock_guard<std::mutex> lock(ctx.mu);
         KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
         cudaStream_t s = o.stream ? static_cast<cudaStream_t>(o.stream) : ctx.stream;
+        ctx.bind(s);
+        if (!o.stream) check_finite_device(s, d_queries, n, index->d, nullptr);
         search_device(ctx, s, d_queries, n, index->dR, index->m, index->d, k, metric, o.path,
                       o.raw_keys, index->base, d_out_dist, d_out_idx,
-                      index_refs(index, n, k, metric, o.path, s));
+                      index_refs(index, n, k, metric, o.path));
         if (!o.stream) KNN_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
@@ -671,14 +704,17 @@ void knn_b200_index_destroy(knn_b200_index* index) { delete index; }
 int knn_b200_last_fallback_count(int device) {
     try {
         DeviceContext& ctx = context_for(device);
-        if (ctx.fb_on_device) {  // resolved on the device by the last search
+        std::lock_guard<std::mutex> lock(ctx.mu);
+        const Scratch* sc = ctx.last;
+        if (!sc) return 0;
+        if (sc->fb_on_device) {  // resolved on the device by the last search
             int v = 0;
             KNN_CUDA_CHECK(cudaSetDevice(ctx.device));
             KNN_CUDA_CHECK(cudaDeviceSynchronize());
-            KNN_CUDA_CHECK(cudaMemcpy(&v, ctx.fb_dev, sizeof(int), cudaMemcpyDeviceToHost));
+            KNN_CUDA_CHECK(cudaMemcpy(&v, sc->fb_dev, sizeof(int), cudaMemcpyDeviceToHost));
             return v;
         }
-        return ctx.last_fallbacks;
+        return sc->last_fallbacks;
     } catch (...) {
         return -1;
     }
@@ -693,6 +729,7 @@ knn_b200_status knn_b200_merge_device(const float* d_part_keys, const int64_t* d
         DeviceContext& ctx = context_for(-1);
         std::lock_guard<std::mutex> lock(ctx.mu);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx.stream;
+        ctx.bind(s);
         MergeArgs mg{};
         mg.part_key = d_part_keys;
         mg.part_idx = d_part_idx;
@@ -707,8 +744,8 @@ knn_b200_status knn_b200_merge_device(const float* d_part_keys, const int64_t* d
             Sizer sz;
             sz.take<float>(static_cast<size_t>(n) * k);
             sz.take<int64_t>(static_cast<size_t>(n) * k);
-            ctx.arena.reserve(sz.used + 256);
-            Carver cv{static_cast<char*>(ctx.arena.base())};
+            ctx.s->arena.reserve(sz.used + 256);
+            Carver cv{static_cast<char*>(ctx.s->arena.base())};
             mg.glist_key = cv.take<float>(static_cast<size_t>(n) * k);
             mg.glist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
         }

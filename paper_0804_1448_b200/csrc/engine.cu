@@ -23,19 +23,48 @@ namespace knnb200 {
 
 DeviceArena::~DeviceArena() {
     if (base_) cudaFree(base_);
+    for (void* p : retired_) cudaFree(p);
+}
+
+namespace {
+thread_local bool t_capturing = false;  // the bound stream is being captured into a graph
 }
 
 void DeviceArena::reserve(size_t bytes) {
+    if (t_capturing) captured_ = true;
     if (bytes <= cap_) return;
+    if (t_capturing)
+        throw CudaError("knn_b200: scratch would have to grow during CUDA graph capture; run the "
+                        "same search once outside the capture first");
+    const size_t want = std::max(bytes, cap_ + cap_ / 2);
     if (base_) {
-        KNN_CUDA_CHECK(cudaDeviceSynchronize());
-        KNN_CUDA_CHECK(cudaFree(base_));
+        if (captured_) {
+            retired_.push_back(base_);  // a captured graph may still replay on it
+        } else {
+            KNN_CUDA_CHECK(cudaDeviceSynchronize());
+            KNN_CUDA_CHECK(cudaFree(base_));
+        }
         base_ = nullptr;
         cap_ = 0;
     }
-    const size_t want = std::max(bytes, cap_ + cap_ / 2);
     KNN_CUDA_CHECK(cudaMalloc(&base_, want));
     cap_ = want;
+}
+
+Scratch::~Scratch() {
+    if (fb_dev) cudaFree(fb_dev);
+}
+
+Scratch& DeviceContext::bind(cudaStream_t st) {
+    auto& slot = scratch[st];
+    if (!slot) slot = std::make_unique<Scratch>();
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    KNN_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+    t_capturing = cs != cudaStreamCaptureStatusNone;
+    if (!slot->fb_dev && !t_capturing) KNN_CUDA_CHECK(cudaMalloc(&slot->fb_dev, sizeof(int)));
+    s = slot.get();
+    last = s;
+    return *s;
 }
 
 DeviceContext& context_for(int device) {
@@ -95,8 +124,8 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
         sz.take<float>(static_cast<size_t>(n) * k);
         sz.take<int64_t>(static_cast<size_t>(n) * k);
     }
-    ctx.arena.reserve(sz.used + 256);
-    Carver cv{static_cast<char*>(ctx.arena.base())};
+    ctx.s->arena.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.s->arena.base())};
     a.part_key = cv.take<float>(part);
     a.part_idx = cv.take<int64_t>(part);
     if (big_k) {

@@ -4,22 +4,42 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
 namespace knnb200 {
 
-// Grow-only device scratch arena (one per context).  Carves aligned slices
-// out of one allocation so a search does a single cudaMalloc at most.
+// Grow-only device scratch arena.  Carves aligned slices out of one
+// allocation so a search does a single cudaMalloc at most.  A block that a
+// captured CUDA graph may reference is never freed while the context lives
+// (growing retires it instead), and the arena cannot grow during a capture.
 class DeviceArena {
 public:
     ~DeviceArena();
     void reserve(size_t bytes);
     void* base() const { return base_; }
+    void mark_captured() { captured_ = true; }
 
 private:
     void* base_ = nullptr;
     size_t cap_ = 0;
+    bool captured_ = false;
+    std::vector<void*> retired_;
+};
+
+// Per-stream scratch of a context: searches on different streams run
+// concurrently and must not share scratch; searches on one stream are
+// ordered by the stream, so they reuse it.
+struct Scratch {
+    DeviceArena arena;       // per-search scratch
+    DeviceArena io;          // host-API staging of inputs / outputs
+    DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
+    int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
+    int* fb_dev = nullptr;   // ... the same count, when resolved on the device
+    bool fb_on_device = false;
+    ~Scratch();
 };
 
 struct Carver {
@@ -50,13 +70,12 @@ struct DeviceContext {
     cudaStream_t copy_stream = nullptr;   // host API: H2D / D2H overlapped with compute
     cudaEvent_t ev[16] = {};              // host API pipeline events
     std::vector<cudaEvent_t> pipe_ev;     // per-chunk events of the pipelined host search
-    DeviceArena arena;       // per-search scratch
-    DeviceArena io;          // host-API staging of inputs / outputs
-    DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
-    std::mutex mu;           // one search at a time per context
-    int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
-    int* fb_dev = nullptr;     // ... the same count, when resolved on the device
-    bool fb_on_device = false;
+    std::mutex mu;           // serializes the host-side enqueue of searches
+    std::map<cudaStream_t, std::unique_ptr<Scratch>> scratch;
+    Scratch* s = nullptr;     // scratch of the stream bound by the current call
+    Scratch* last = nullptr;  // scratch of the last search (fallback count)
+    // Select (create) the scratch of `stream` for the calling search (under mu).
+    Scratch& bind(cudaStream_t stream);
 };
 
 DeviceContext& context_for(int device);  // device < 0: current device

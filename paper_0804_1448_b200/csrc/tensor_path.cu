@@ -105,9 +105,9 @@ void tensor_prep_refs(cudaStream_t stream, const float* dR, int64_t m, int d, vo
 void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
                      float* d_out, int64_t* d_idx) {
-    ctx.refs.reserve(tensor_refs_bytes(m, d));
+    ctx.s->refs.reserve(tensor_refs_bytes(m, d));
     TensorRefs r;
-    tensor_prep_refs(stream, dR, m, d, ctx.refs.base(), r);
+    tensor_prep_refs(stream, dR, m, d, ctx.s->refs.base(), r);
     tensor_search(ctx, stream, r, dQ, n, k, raw_keys, index_base, d_out, d_idx);
 }
 
@@ -164,14 +164,11 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     sz.take<int>(static_cast<size_t>(pairs));
     // small k: the certification fallback runs on the device (exact kernel over
     // the failed queries, count read on the device): its partial-list slots
-    const int fb_ctas = exact_max_ctas(k, true);
-    const size_t fb_part = large ? 0
-                                 : static_cast<size_t>(exact_slots(n, exact_ntiles(m), fb_ctas)) *
-                                       exact_queries_per_cta() * k;
+    const size_t fb_part = large ? 0 : fallback_part_elems(n, m, k);
     sz.take<float>(fb_part);
     sz.take<int64_t>(fb_part);
-    ctx.arena.reserve(sz.used + 256);
-    Carver cv{static_cast<char*>(ctx.arena.base())};
+    ctx.s->arena.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.s->arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
     __half* Rh = refs.Rh;
     const float* rnorm = refs.rnorm;
@@ -339,11 +336,28 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     if (!large) launch_rerank(ra, rr_smem, stream);
 
     // 4. certification fallback (exact kernel on the failed queries), unless
-    //    the caller collects them across several searches.  Small k: entirely
-    //    on the device -- no host round trip, the search stays asynchronous.
+    //    the caller collects them across several searches.
     if (sink) return;
-    if (!ctx.fb_dev) KNN_CUDA_CHECK(cudaMalloc(&ctx.fb_dev, sizeof(int)));
-    if (!large) {
+    tensor_resolve_fallbacks(ctx, stream, refs, dQ, n, k, raw_keys, index_base, d_out, d_idx, fb,
+                             fb_pk, fb_pi, margin, retry);
+}
+
+size_t fallback_part_elems(int64_t n, int64_t m, int k) {
+    return static_cast<size_t>(exact_slots(n, exact_ntiles(m), exact_max_ctas(k, true))) *
+           exact_queries_per_cta() * k;
+}
+
+void tensor_resolve_fallbacks(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
+                              const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
+                              float* d_out, int64_t* d_idx, int* fb, float* fb_pk, int64_t* fb_pi,
+                              int margin, bool retry) {
+    const float* dR = refs.dR;
+    const int64_t m = refs.m;
+    const int d = refs.d;
+    // Small k: entirely on the device -- the exact kernel reads the failed
+    // query list and its count from HBM (fixed grid), no host round trip, so
+    // the search stays asynchronous and graph-capturable.
+    if (k <= MAX_KQ) {
         ExactArgs ea{};
         ea.Q = dQ;
         ea.R = dR;
@@ -361,19 +375,19 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         ea.part_key = fb_pk;
         ea.part_idx = fb_pi;
         launch_exact(kL2, ea, stream);
-        KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        ctx.fb_on_device = true;
+        if (ctx.s->fb_dev)
+            KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        ctx.s->fb_on_device = true;
         return;
     }
-    ctx.fb_on_device = false;
+    ctx.s->fb_on_device = false;
     int fails = 0;
     KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
     KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
     if (fails > 0) {
-        std::vector<int> list(static_cast<size_t>(fails));
-        KNN_CUDA_CHECK(cudaMemcpy(list.data(), fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToHost));
         // the fallback allocates its own scratch: keep the gathered queries in a
         // dedicated buffer so the exact path's arena use cannot clobber them
+        // (the list too: fb may live in the arena the nested search reuses)
         float* gq = nullptr;
         float* od = nullptr;
         int64_t* oi = nullptr;
@@ -382,21 +396,20 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         KNN_CUDA_CHECK(cudaMallocAsync(&od, sizeof(float) * fails * k, stream));
         KNN_CUDA_CHECK(cudaMallocAsync(&oi, sizeof(int64_t) * fails * k, stream));
         KNN_CUDA_CHECK(cudaMallocAsync(&dl, sizeof(int) * fails, stream));
-        KNN_CUDA_CHECK(cudaMemcpyAsync(dl, list.data(), sizeof(int) * fails, cudaMemcpyHostToDevice,
-                                       stream));
+        KNN_CUDA_CHECK(cudaMemcpyAsync(dl, fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToDevice, stream));
         launch_gather_rows(dQ, d, dl, fails, gq, stream);
-        if (large && !retry)  // a tail estimate of T0: once more from fresh seed tiles
+        if (!retry)  // a tail estimate of T0: once more from fresh seed tiles
             tensor_search(ctx, stream, refs, gq, fails, k, raw_keys, index_base, od, oi, nullptr,
                           margin, true);
         else
             run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
         launch_scatter_rows(od, oi, dl, fails, k, d_out, d_idx, stream);
+        KNN_CUDA_CHECK(cudaFreeAsync(dl, stream));
         KNN_CUDA_CHECK(cudaFreeAsync(gq, stream));
         KNN_CUDA_CHECK(cudaFreeAsync(od, stream));
         KNN_CUDA_CHECK(cudaFreeAsync(oi, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(dl, stream));
     }
-    ctx.last_fallbacks = fails;
+    ctx.s->last_fallbacks = fails;
 }
 
 }  // namespace knnb200

@@ -49,6 +49,16 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
                    float* d_out, int64_t* d_idx, const FallbackSink* sink = nullptr,
                    int margin = 3, bool retry = false);
 
+// Resolve the certification fallbacks recorded in fb ({count, query list}) of
+// a search over dQ (n rows): small k on the device (exact kernel over the
+// list; fb_pk / fb_pi: fallback_part_elems(n, m, k) partial-list slots), large
+// k host-driven (one re-seeded retry, then the exact path).
+size_t fallback_part_elems(int64_t n, int64_t m, int k);
+void tensor_resolve_fallbacks(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
+                              const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
+                              float* d_out, int64_t* d_idx, int* fb, float* fb_pk, int64_t* fb_pi,
+                              int margin = 3, bool retry = false);
+
 // exact path on a subset of queries (certification fallback), defined in engine.cu
 void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                       const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,

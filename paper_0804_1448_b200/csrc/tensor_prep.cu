@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
          row += wstep) {
         const bool real = row < a.rows;
         double h2 = 0.0, e2 = 0.0;
+        bool ovf = false;  // a query operand -2 h overflowed fp16
         __half* out = a.Xh + row * a.Kp;
         float xv[5];  // this lane's coordinates, all loads in flight at once (Kp <= 160)
 #pragma unroll
@@ -151,7 +152,10 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
                 const double err = fabs(hv - static_cast<double>(t)) + fabs(static_cast<double>(t)) * 0x1.0p-23;
                 h2 += hv * hv;
                 e2 += err * err;
-                if (QUERY) h = __float2half_rn(-2.f * __half2float(h));  // exact: power-of-two scale
+                if (QUERY) {  // exact (power-of-two scale) unless -2 h leaves the fp16 range
+                    h = __float2half_rn(-2.f * __half2float(h));
+                    ovf |= __hisinf(h) != 0;
+                }
             }
             out[c] = h;
         }
@@ -160,7 +164,11 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
             h2 += __shfl_xor_sync(0xffffffffu, h2, o);
             e2 += __shfl_xor_sync(0xffffffffu, e2, o);
         }
-        const float delta = static_cast<float>(sqrt(e2) * (1.0 + 0x1.0p-20)) * (1.f + 1e-6f);
+        // an overflowed operand breaks the MMA's error model: an infinite
+        // rounding radius makes every bound infinite, so the query fails the
+        // certificate and is recomputed exactly
+        const bool any_ovf = __any_sync(0xffffffffu, ovf);
+        const float delta = any_ovf ? kInf : static_cast<float>(sqrt(e2) * (1.0 + 0x1.0p-20)) * (1.f + 1e-6f);
         const float xn = static_cast<float>(sqrt(h2)) * (1.f + 1e-6f);
         if (lane == 0) {
             if (QUERY) {
