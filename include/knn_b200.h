@@ -150,6 +150,55 @@ KNN_B200_API knn_b200_status knn_b200_merge_device(const float *d_part_keys, con
                                       int32_t parts, int64_t n, int32_t k, int32_t metric,
                                       void *stream, float *d_out_dist, int64_t *d_out_idx);
 
+/* ---- multi-GPU (north star (4)) --------------------------
+ * The reference scans all m references per query in one process
+ * (bruteforce.cpp:24-29,81-96); here the m axis (or the query axis) is split
+ * over GPUs.  Reference-sharded: device g holds the contiguous rows
+ * [g m / G, (g+1) m / G) and all queries, the per-device n x k lists are
+ * all-gathered over NCCL and merged on the device -- bitwise one search over
+ * all of R.  Query-sharded: every device holds R and searches its rows of Q;
+ * no collective.  NCCL (libnccl.so.2) is loaded at first use; its failures
+ * are KNN_B200_ENCCL. */
+typedef enum knn_b200_shard_mode {
+    KNN_B200_SHARD_REFERENCES = 0,
+    KNN_B200_SHARD_QUERIES = 1
+} knn_b200_shard_mode;
+
+/* One process driving G devices (devices NULL = 0..G-1): host R is uploaded
+ * shard by shard (each shard prepared once, like knn_b200_index_create). */
+typedef struct knn_b200_sharded knn_b200_sharded;
+KNN_B200_API knn_b200_status knn_b200_sharded_create(const float *references, int64_t m,
+                                                     int32_t d, int32_t num_devices,
+                                                     const int32_t *devices, int32_t shard_mode,
+                                                     const knn_b200_options *opt,
+                                                     knn_b200_sharded **out);
+/* Host queries in, host n x k table out (bf_knn layout). */
+KNN_B200_API knn_b200_status knn_b200_sharded_search(knn_b200_sharded *h, const float *queries,
+                                                     int64_t n, int32_t k, int32_t metric,
+                                                     const knn_b200_options *opt,
+                                                     float *out_dist, int64_t *out_idx);
+KNN_B200_API void knn_b200_sharded_destroy(knn_b200_sharded *h);
+
+/* One process per GPU (e.g. torchrun): rank 0 creates the NCCL unique id
+ * (len >= 128 bytes), the caller broadcasts it, every rank creates its
+ * communicator, builds an index over its own shard (index_base = its first
+ * global row) and calls knn_b200_dist_search_device with the same queries:
+ * local search, NCCL all-gather of the raw-key lists, device merge -- every
+ * rank receives the final n x k table in its device buffers. */
+typedef struct knn_b200_comm knn_b200_comm;
+KNN_B200_API knn_b200_status knn_b200_nccl_unique_id(void *out, size_t len);
+KNN_B200_API int knn_b200_nccl_version(void);
+KNN_B200_API knn_b200_status knn_b200_comm_create(const void *unique_id, size_t len,
+                                                  int32_t nranks, int32_t rank, int32_t device,
+                                                  knn_b200_comm **out);
+KNN_B200_API void knn_b200_comm_destroy(knn_b200_comm *comm);
+KNN_B200_API knn_b200_status knn_b200_dist_search_device(knn_b200_comm *comm,
+                                                         knn_b200_index *local_shard,
+                                                         const float *d_queries, int64_t n,
+                                                         int32_t k, int32_t metric,
+                                                         const knn_b200_options *opt,
+                                                         float *d_out_dist, int64_t *d_out_idx);
+
 /* Number of CUDA kernels this library launched on the calling thread since
  * the last reset (for bench.py's gpu_launches accounting). */
 KNN_B200_API uint64_t knn_b200_launch_count(void);

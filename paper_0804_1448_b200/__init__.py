@@ -24,7 +24,8 @@ __all__ = [
     "BfConfig", "SearchStats", "Metric", "NeighborTable", "bf_knn", "search_device",
     "Index", "merge_device", "library", "lib_path", "KnnError", "PATH_AUTO", "PATH_EXACT",
     "PATH_TENSOR", "launch_count", "reset_launch_count", "profile_enable", "profile_collect",
-    "fill_uniform_device",
+    "fill_uniform_device", "Sharded", "Comm", "nccl_unique_id", "SHARD_REFERENCES",
+    "SHARD_QUERIES",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -41,7 +42,11 @@ EXPORTS = [
     "knn_b200_merge_device", "knn_b200_launch_count", "knn_b200_reset_launch_count",
     "knn_b200_profile_enable", "knn_b200_profile_only", "knn_b200_profile_collect", "knn_b200_fill_uniform_device",
     "knn_b200_last_fallback_count", "knn_b200_debug_mma_probe",
+    "knn_b200_sharded_create", "knn_b200_sharded_search", "knn_b200_sharded_destroy",
+    "knn_b200_nccl_unique_id", "knn_b200_nccl_version", "knn_b200_comm_create",
+    "knn_b200_comm_destroy", "knn_b200_dist_search_device",
 ]
+SHARD_REFERENCES, SHARD_QUERIES = 0, 1
 
 
 class KnnError(RuntimeError):
@@ -78,6 +83,15 @@ def library() -> C.CDLL:
     if not os.path.exists(lib_path):
         raise RuntimeError(f"{lib_path} is missing: run `python -c 'import __graft_entry__ as g; "
                            "g.build()'` (there is no CPU fallback)")
+    # NCCL is loaded by the library at first use: point it at the pip NCCL that
+    # PyTorch links (if present), so both share one libnccl.so.2 in the process
+    if "KNN_B200_NCCL_LIB" not in os.environ:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec is not None and spec.submodule_search_locations:
+            cand = os.path.join(list(spec.submodule_search_locations)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["KNN_B200_NCCL_LIB"] = cand
     lib = C.CDLL(lib_path)
     vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
     lib.knn_b200_options_init.argtypes = [C.POINTER(_Options)]
@@ -106,9 +120,22 @@ def library() -> C.CDLL:
     lib.knn_b200_last_fallback_count.argtypes = [C.c_int]
     lib.knn_b200_fill_uniform_device.restype = C.c_int
     lib.knn_b200_fill_uniform_device.argtypes = [vp, i64, C.c_uint64, i64, vp]
+    lib.knn_b200_sharded_create.argtypes = [vp, i64, i32, i32, vp, i32, C.POINTER(_Options),
+                                            C.POINTER(vp)]
+    lib.knn_b200_sharded_search.argtypes = [vp, vp, i64, i32, i32, C.POINTER(_Options), vp, vp]
+    lib.knn_b200_sharded_destroy.argtypes = [vp]
+    lib.knn_b200_nccl_unique_id.argtypes = [vp, C.c_size_t]
+    lib.knn_b200_nccl_version.restype = C.c_int
+    lib.knn_b200_comm_create.argtypes = [vp, C.c_size_t, i32, i32, i32, C.POINTER(vp)]
+    lib.knn_b200_comm_destroy.argtypes = [vp]
+    lib.knn_b200_dist_search_device.argtypes = [vp, vp, vp, i64, i32, i32, C.POINTER(_Options),
+                                                vp, vp]
     for name in ("knn_b200_search", "knn_b200_search_device", "knn_b200_index_create",
                  "knn_b200_index_create_device", "knn_b200_index_search",
-                 "knn_b200_index_search_device", "knn_b200_merge_device"):
+                 "knn_b200_index_search_device", "knn_b200_merge_device",
+                 "knn_b200_sharded_create", "knn_b200_sharded_search",
+                 "knn_b200_nccl_unique_id", "knn_b200_comm_create",
+                 "knn_b200_dist_search_device"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -159,6 +186,9 @@ def _check(status: int) -> None:
     if status == 1:
         raise ValueError(msg)
     raise KnnError(status, msg)
+
+
+NCCL_ID_BYTES = 128
 
 
 # --------------------------------------------------------------- mirror types
@@ -375,3 +405,94 @@ class Index:
             self.close()
         except Exception:
             pass
+
+
+class Sharded:
+    """One process, several GPUs: the reference set split into
+    contiguous shards (``mode=SHARD_REFERENCES``: per-device top-k, NCCL
+    all-gather, device merge -- bitwise one search over all of R) or the
+    queries split over devices that each hold all of R (``SHARD_QUERIES``)."""
+
+    def __init__(self, references, num_devices: int, mode: int = SHARD_REFERENCES,
+                 devices=None):
+        R = _as_points(references)
+        self.m, self.d = R.shape
+        self.num_devices = int(num_devices)
+        h = C.c_void_p()
+        devs = None
+        if devices is not None:
+            devs = (C.c_int32 * len(devices))(*devices)
+        o = _opts()
+        _check(library().knn_b200_sharded_create(R.ctypes.data, self.m, self.d, self.num_devices,
+                                                 C.cast(devs, C.c_void_p) if devs else None,
+                                                 int(mode), C.byref(o), C.byref(h)))
+        self._h = h
+
+    def search(self, queries, k: int, metric: int = EUCLIDEAN,
+               path: int = PATH_AUTO) -> NeighborTable:
+        Q = _as_points(queries)
+        n = Q.shape[0]
+        out_d = np.empty((n, k), np.float32)
+        out_i = np.empty((n, k), np.int64)
+        o = _opts(BfConfig(path=path))
+        _check(library().knn_b200_sharded_search(self._h, Q.ctypes.data, n, int(k), metric,
+                                                 C.byref(o), out_d.ctypes.data,
+                                                 out_i.ctypes.data))
+        return NeighborTable(out_i, out_d)
+
+    def close(self) -> None:
+        if self._h:
+            library().knn_b200_sharded_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(library().knn_b200_nccl_unique_id(buf, NCCL_ID_BYTES))
+    return buf.raw
+
+
+class Comm:
+    """One rank of a one-process-per-GPU job (e.g. under torchrun): the NCCL
+    communicator the reference-sharded search all-gathers over."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, device: int):
+        if len(unique_id) < NCCL_ID_BYTES:
+            raise ValueError("Comm: unique id must hold 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id[:NCCL_ID_BYTES]), NCCL_ID_BYTES)
+        h = C.c_void_p()
+        _check(library().knn_b200_comm_create(buf, NCCL_ID_BYTES, nranks, rank, device,
+                                              C.byref(h)))
+        self._h = h
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def search_device(self, shard: "Index", q_ptr: int, n: int, k: int, out_dist_ptr: int,
+                      out_idx_ptr: int, metric: int = EUCLIDEAN, path: int = PATH_AUTO,
+                      stream: int = 0) -> None:
+        """This rank's shard search + NCCL all-gather + device merge: every rank
+        receives the final n x k table over all shards."""
+        o = _opts(BfConfig(path=path), stream=stream)
+        _check(library().knn_b200_dist_search_device(self._h, shard._h, q_ptr, n, int(k), metric,
+                                                     C.byref(o), out_dist_ptr, out_idx_ptr))
+
+    def close(self) -> None:
+        if self._h:
+            library().knn_b200_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_version() -> int:
+    return int(library().knn_b200_nccl_version())

@@ -28,28 +28,9 @@ namespace {
 thread_local std::string g_last_error;
 thread_local uint64_t g_launches = 0;
 
-knn_b200_status fail(knn_b200_status s, const std::string& msg) {
-    g_last_error = msg;
-    return s;
-}
-
 template <typename F>
 knn_b200_status guarded(F&& body) {
-    try {
-        g_last_error.clear();
-        body();
-        return KNN_B200_OK;
-    } catch (const InvalidArgument& e) {
-        return fail(KNN_B200_EINVAL, e.what());
-    } catch (const OutOfMemory& e) {
-        return fail(KNN_B200_ENOMEM, e.what());
-    } catch (const CudaError& e) {
-        return fail(KNN_B200_ECUDA, e.what());
-    } catch (const std::bad_alloc& e) {
-        return fail(KNN_B200_ENOMEM, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(KNN_B200_EINTERNAL, e.what());
-    }
+    return static_cast<knn_b200_status>(abi_guarded(std::forward<F>(body)));
 }
 
 const knn_b200_options& opts_or_default(const knn_b200_options* opt, knn_b200_options& tmp) {
@@ -236,6 +217,8 @@ void check_search(int64_t dq, int64_t dr, int64_t m, int64_t k, const knn_b200_o
 }  // namespace
 
 void note_launch(int count) { g_launches += static_cast<uint64_t>(count); }
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 }  // namespace knnb200
 

@@ -25,6 +25,39 @@ struct CudaError : std::runtime_error {
 struct OutOfMemory : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// The C ABI's error convention (capi.cu): run `body`, map exceptions to
+// status codes, keep the message for knn_b200_last_error() (thread-local).
+void set_last_error(const std::string& msg);
+template <typename F>
+int abi_guarded(F&& body) {
+    try {
+        set_last_error("");
+        body();
+        return 0;                                               // KNN_B200_OK
+    } catch (const InvalidArgument& e) {
+        set_last_error(e.what());
+        return 1;                                               // KNN_B200_EINVAL
+    } catch (const OutOfMemory& e) {
+        set_last_error(e.what());
+        return 2;                                               // KNN_B200_ENOMEM
+    } catch (const CudaError& e) {
+        set_last_error(e.what());
+        return 3;                                               // KNN_B200_ECUDA
+    } catch (const NcclError& e) {
+        set_last_error(e.what());
+        return 4;                                               // KNN_B200_ENCCL
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return 2;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return 5;                                               // KNN_B200_EINTERNAL
+    }
+}
 
 void note_launch(int count = 1);  // launch accounting (capi.cpp)
 
