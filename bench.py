@@ -391,6 +391,8 @@ def run_line(be, plumb, letter, cfg, args, world, rank, path):
     if world > 1:
         uid = plumb.broadcast_bytes(be.unique_id() if rank == 0 else None)
         comm = be.comm(uid, world, rank)
+    elif os.environ.get("KNN_BENCH_FORCE_DIST"):  # dev: the N > 1 step on a 1-rank communicator
+        comm = be.comm(be.unique_id(), 1, 0)
 
     def step():
         if comm is None:
@@ -494,6 +496,65 @@ def run_line(be, plumb, letter, cfg, args, world, rank, path):
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "correctness_gate": gate, "clocks": clocks.summary(),
     }
+
+
+def run_rho_line(be, letter, cfg, args):
+    """--task rho_k: the entropy estimator's self-join (entropy.cpp:75-89,
+    rho_k_all) on the config's reference set: one device search of every
+    point against the set with k + 1, self excluded by index in the epilogue.
+    value = points/s."""
+    torch, knn = be.torch, be.knn
+    m, d, k = cfg["m"], cfg["d"], cfg["k"]
+    sr, _ = seeds(cfg)
+    P = be.empty((m, d))
+    be.fill_uniform(P, sr, 0)
+    out = torch.empty(m, dtype=torch.float64, device=be.dev)
+    step = lambda: knn.rho_k_all_device(P.data_ptr(), m, d, k, out.data_ptr(), stream=be.sptr)
+    for _ in range(args.warmup):
+        step()
+    be.sync()
+    ev = [(be.event(), be.event()) for _ in range(args.steps)]
+    be.reset_launch_count()
+    for a, b in ev:
+        be.flush_l2()
+        be.record(a)
+        step()
+        be.record(b)
+    be.sync()
+    launches = be.launch_count()
+    ms = sum(be.elapsed_ms(a, b) for a, b in ev) / args.steps
+    got = out.cpu().numpy()
+    from oracle.oracle import Oracle, Reference
+    orc = Oracle()
+    Ph = orc.counter_f32(m, d, sr)
+    pick = np.linspace(0, m - 1, 256).astype(np.int64)
+    ri, rd = orc.knn(Ph[pick], Ph, k + 1)
+    want = np.array([[x for j, x in zip(ri[t], rd[t]) if j != pick[t]][k - 1]
+                     for t in range(len(pick))])
+    ok = bool(np.allclose(got[pick], want, rtol=1e-5, atol=0))
+    if not ok:
+        print(json.dumps({"error": "rho_k correctness gate failed"}), file=sys.stderr)
+        sys.exit(1)
+    cpu = None
+    if not args.no_cpu_baseline:
+        ref = Reference()
+        s = 2000
+        t0 = time.perf_counter()
+        ref.bf_knn(Ph[:s].astype(np.float64), Ph.astype(np.float64), k + 1)
+        t = time.perf_counter() - t0
+        cpu = {"value": round(s / t, 2), "unit": "points/s", "cores": ref.max_threads(),
+               "kind": "reference", "sample": f"knn::bf_knn(first {s} points, all {m}, k+1={k + 1}), "
+               "the search inside knn::rho_k_all (entropy.cpp:84)"}
+    return {"metric": "rho_k_all points/sec (self-join, entropy.cpp:75-89)",
+            "value": round(m / (ms / 1e3), 1), "unit": "points/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"rho_k_all over {workload_name(letter, cfg)} points",
+                       "n": m, "d": d, "k": k, "task": "rho_k"},
+            "gpu_launches": launches, "cpu_baseline": cpu,
+            "correctness_gate": {"points_checked": 256, "result": "pass",
+                                 "oracle": "oracle/knn_oracle.c k+1 search, self dropped by index"}}
 
 
 def correctness_gate(cfg, oi, od, sr, sq, sample: int = 256):
@@ -711,6 +772,10 @@ def run_ours(args, letter):
         dist.init_process_group("nccl", device_id=be.dev)
         plumb = DistPlumbing(world, rank, "nccl")
     path = {"auto": 0, "exact": 1, "tensor": 2}[args.path]
+    if args.task == "rho_k":
+        for cfg in CONFIGS[letter][1]:
+            print(json.dumps(run_rho_line(be, letter, cfg, args)), flush=True)
+        return
     for cfg in CONFIGS[letter][1]:
         line = run_line(be, plumb, letter, cfg, args, world, rank, path)
         if line is not None:
@@ -729,6 +794,8 @@ def parse(argv=None):
     ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
                     help="BASELINE.json config (default: B on 1 GPU, E on N > 1)")
     ap.add_argument("--path", choices=["auto", "exact", "tensor"], default="auto")
+    ap.add_argument("--task", choices=["search", "rho_k"], default="search",
+                    help="rho_k: the entropy self-join (rho_k_all) on the config's points")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args(argv)

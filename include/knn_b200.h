@@ -199,6 +199,38 @@ KNN_B200_API knn_b200_status knn_b200_dist_search_device(knn_b200_comm *comm,
                                                          const knn_b200_options *opt,
                                                          float *d_out_dist, int64_t *d_out_idx);
 
+/* ---- the hot path's next consumers, on the device
+ * One engine search + an epilogue kernel over the table in HBM. */
+
+/* entropy.cpp:75-89 rho_k_all: for every point, the Euclidean distance to its
+ * k-th nearest OTHER point (self excluded by index; coincident points count
+ * at distance 0).  Error text as the reference ("rho_k_all: k = K needs at
+ * least k + 1 points, set has N"). */
+KNN_B200_API knn_b200_status knn_b200_rho_k_all(const float *points, int64_t n, int32_t d,
+                                                int32_t k, const knn_b200_options *opt,
+                                                double *out_rho);
+KNN_B200_API knn_b200_status knn_b200_rho_k_all_device(const float *d_points, int64_t n,
+                                                       int32_t d, int32_t k,
+                                                       const knn_b200_options *opt,
+                                                       double *d_out_rho);
+/* applications.cpp:36-63 knn_classify: majority label of the k nearest training
+ * points; vote ties by the smaller summed distance, then the smaller label. */
+KNN_B200_API knn_b200_status knn_b200_knn_classify(const float *train, int64_t m, int32_t d,
+                                                   const int64_t *labels, const float *queries,
+                                                   int64_t n, int32_t dq, int32_t k,
+                                                   int32_t metric, const knn_b200_options *opt,
+                                                   int64_t *out_labels);
+/* applications.cpp:65-86 retrieve_vote: every query descriptor's k nearest
+ * database descriptors vote for their owning image; scores[image_count] and
+ * the ranking (descending score, ties by ascending id).  DescriptorDatabase
+ * validation and messages as applications.cpp:9-34. */
+KNN_B200_API knn_b200_status knn_b200_retrieve_vote(const float *descriptors, int64_t m,
+                                                    int32_t d, const int64_t *image_of,
+                                                    int64_t image_count, const float *queries,
+                                                    int64_t n, int32_t dq, int32_t k,
+                                                    int32_t metric, const knn_b200_options *opt,
+                                                    uint64_t *out_scores, int64_t *out_ranking);
+
 /* Number of CUDA kernels this library launched on the calling thread since
  * the last reset (for bench.py's gpu_launches accounting). */
 KNN_B200_API uint64_t knn_b200_launch_count(void);

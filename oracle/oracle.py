@@ -147,6 +147,14 @@ class Reference:
         lib.knnref_rho_k_all.restype = C.c_int
         lib.knnref_rho_k_all.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp,
                                          C.c_char_p, C.c_size_t]
+        lib.knnref_knn_classify.restype = C.c_int
+        lib.knnref_knn_classify.argtypes = [_dp, C.c_size_t, C.c_size_t, _ip, C.c_size_t, _dp,
+                                            C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, _ip,
+                                            C.c_char_p, C.c_size_t]
+        lib.knnref_retrieve_vote.restype = C.c_int
+        lib.knnref_retrieve_vote.argtypes = [_dp, C.c_size_t, C.c_size_t, _ip, C.c_size_t,
+                                             C.c_int64, _dp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                             C.c_int, _up, _ip, C.c_char_p, C.c_size_t]
         lib.knnref_derive_seed.restype = C.c_uint64
         lib.knnref_derive_seed.argtypes = [C.c_uint64] * 4
         lib.knnref_uniform.argtypes = [C.c_uint64, _dp, C.c_size_t]
@@ -200,6 +208,38 @@ class Reference:
         if self.lib.knnref_rho_k_all(P, P.shape[0], P.shape[1], k, out, err, 512) != 0:
             raise ValueError(err.value.decode())
         return out
+
+    def knn_classify(self, T, labels, Q, k: int, metric: int = EUCLIDEAN):
+        """applications.cpp:36-63 (the reference's own knn_classify)."""
+        T = np.ascontiguousarray(T, np.float64)
+        Q = np.ascontiguousarray(Q, np.float64)
+        lab = np.ascontiguousarray(labels, np.int64)
+        out = np.empty(Q.shape[0], np.int64)
+        err = C.create_string_buffer(512)
+        s = self.lib.knnref_knn_classify(T, T.shape[0], T.shape[1], lab, lab.size, Q, Q.shape[0],
+                                         Q.shape[1], k, metric, out, err, 512)
+        if s == 1:
+            raise ValueError(err.value.decode())
+        if s != 0:
+            raise ReferenceError_(err.value.decode())
+        return out
+
+    def retrieve_vote(self, D, image_of, images: int, Q, k: int, metric: int = EUCLIDEAN):
+        """applications.cpp:65-86 (the reference's own retrieve_vote)."""
+        D = np.ascontiguousarray(D, np.float64)
+        Q = np.ascontiguousarray(Q, np.float64)
+        own = np.ascontiguousarray(image_of, np.int64)
+        scores = np.empty(max(images, 1), np.uint64)
+        ranking = np.empty(max(images, 1), np.int64)
+        err = C.create_string_buffer(512)
+        s = self.lib.knnref_retrieve_vote(D, D.shape[0], D.shape[1], own, own.size, images, Q,
+                                          Q.shape[0], Q.shape[1], k, metric, scores, ranking,
+                                          err, 512)
+        if s == 1:
+            raise ValueError(err.value.decode())
+        if s != 0:
+            raise ReferenceError_(err.value.decode())
+        return scores[:images], ranking[:images]
 
     def derive_seed(self, master: int, a: int, b: int = 0, c: int = 0) -> int:
         return int(self.lib.knnref_derive_seed(master, a, b, c))

@@ -11,6 +11,7 @@
 //   knn::bf_knn          include/knn/bruteforce.hpp:31-33
 //   knn::reference_knn   include/knn/reference.hpp:15-16
 //   knn::rho_k_all       include/knn/entropy.hpp (self-join caller of bf_knn)
+//   knn::knn_classify / knn::retrieve_vote   include/knn/applications.hpp
 //   knn::derive_seed / next_unit   include/knn/rng.hpp:17-38
 #include <cstdint>
 #include <cstring>
@@ -22,6 +23,7 @@
 
 #include <omp.h>
 
+#include "knn/applications.hpp"
 #include "knn/bruteforce.hpp"
 #include "knn/entropy.hpp"
 #include "knn/metric.hpp"
@@ -117,6 +119,47 @@ int knnref_rho_k_all(const double* P, std::size_t n, std::size_t d, std::size_t 
     } catch (const std::exception& e) {
         copy_err(e, err, errlen);
         return 1;
+    }
+}
+
+int knnref_knn_classify(const double* T, std::size_t m, std::size_t dt, const std::int64_t* labels,
+                        std::size_t nlabels, const double* Q, std::size_t n, std::size_t dq,
+                        std::size_t k, int metric, std::int64_t* out, char* err,
+                        std::size_t errlen) {
+    try {
+        knn::LabeledSet train(knn::PointSet(m, dt, std::vector<double>(T, T + m * dt)),
+                              std::vector<std::int64_t>(labels, labels + nlabels));
+        knn::PointSet q(n, dq, std::vector<double>(Q, Q + n * dq));
+        const auto r = knn::knn_classify(train, q, k, make_metric(metric, dq, nullptr));
+        std::memcpy(out, r.data(), n * sizeof(std::int64_t));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        copy_err(e, err, errlen);
+        return 1;
+    } catch (const std::exception& e) {
+        copy_err(e, err, errlen);
+        return 2;
+    }
+}
+
+int knnref_retrieve_vote(const double* D, std::size_t m, std::size_t dd, const std::int64_t* owners,
+                         std::size_t nowners, std::int64_t images, const double* Q, std::size_t n,
+                         std::size_t dq, std::size_t k, int metric, std::uint64_t* scores,
+                         std::int64_t* ranking, char* err, std::size_t errlen) {
+    try {
+        knn::DescriptorDatabase db(knn::PointSet(m, dd, std::vector<double>(D, D + m * dd)),
+                                   std::vector<std::int64_t>(owners, owners + nowners), images);
+        knn::PointSet q(n, dq, std::vector<double>(Q, Q + n * dq));
+        const knn::VoteTally t = knn::retrieve_vote(db, q, k, make_metric(metric, dq, nullptr));
+        std::memcpy(scores, t.scores.data(), t.scores.size() * sizeof(std::uint64_t));
+        std::memcpy(ranking, t.ranking.data(), t.ranking.size() * sizeof(std::int64_t));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        copy_err(e, err, errlen);
+        return 1;
+    } catch (const std::exception& e) {
+        copy_err(e, err, errlen);
+        return 2;
     }
 }
 

@@ -24,7 +24,8 @@ __all__ = [
     "BfConfig", "SearchStats", "Metric", "NeighborTable", "bf_knn", "search_device",
     "Index", "merge_device", "library", "lib_path", "KnnError", "PATH_AUTO", "PATH_EXACT",
     "PATH_TENSOR", "launch_count", "reset_launch_count", "profile_enable", "profile_collect",
-    "fill_uniform_device", "Sharded", "Comm", "nccl_unique_id", "SHARD_REFERENCES",
+    "fill_uniform_device", "Sharded", "Comm", "rho_k_all", "knn_classify", "retrieve_vote",
+    "VoteTally", "nccl_unique_id", "SHARD_REFERENCES",
     "SHARD_QUERIES",
 ]
 
@@ -44,7 +45,8 @@ EXPORTS = [
     "knn_b200_last_fallback_count", "knn_b200_debug_mma_probe",
     "knn_b200_sharded_create", "knn_b200_sharded_search", "knn_b200_sharded_destroy",
     "knn_b200_nccl_unique_id", "knn_b200_nccl_version", "knn_b200_comm_create",
-    "knn_b200_comm_destroy", "knn_b200_dist_search_device",
+    "knn_b200_comm_destroy", "knn_b200_dist_search_device", "knn_b200_rho_k_all",
+    "knn_b200_rho_k_all_device", "knn_b200_knn_classify", "knn_b200_retrieve_vote",
 ]
 SHARD_REFERENCES, SHARD_QUERIES = 0, 1
 
@@ -85,6 +87,7 @@ def library() -> C.CDLL:
                            "g.build()'` (there is no CPU fallback)")
     # NCCL is loaded by the library at first use: point it at the pip NCCL that
     # PyTorch links (if present), so both share one libnccl.so.2 in the process
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's banner off stdout (bench JSON)
     if "KNN_B200_NCCL_LIB" not in os.environ:
         import importlib.util
         spec = importlib.util.find_spec("nvidia.nccl")
@@ -130,6 +133,15 @@ def library() -> C.CDLL:
     lib.knn_b200_comm_destroy.argtypes = [vp]
     lib.knn_b200_dist_search_device.argtypes = [vp, vp, vp, i64, i32, i32, C.POINTER(_Options),
                                                 vp, vp]
+    lib.knn_b200_rho_k_all.argtypes = [vp, i64, i32, i32, C.POINTER(_Options), vp]
+    lib.knn_b200_rho_k_all_device.argtypes = [vp, i64, i32, i32, C.POINTER(_Options), vp]
+    lib.knn_b200_knn_classify.argtypes = [vp, i64, i32, vp, vp, i64, i32, i32, i32,
+                                          C.POINTER(_Options), vp]
+    lib.knn_b200_retrieve_vote.argtypes = [vp, i64, i32, vp, i64, vp, i64, i32, i32, i32,
+                                           C.POINTER(_Options), vp, vp]
+    for name in ("knn_b200_rho_k_all", "knn_b200_rho_k_all_device", "knn_b200_knn_classify",
+                 "knn_b200_retrieve_vote"):
+        getattr(lib, name).restype = C.c_int
     for name in ("knn_b200_search", "knn_b200_search_device", "knn_b200_index_create",
                  "knn_b200_index_create_device", "knn_b200_index_search",
                  "knn_b200_index_search_device", "knn_b200_merge_device",
@@ -496,3 +508,70 @@ class Comm:
 
 def nccl_version() -> int:
     return int(library().knn_b200_nccl_version())
+
+
+# ------------------------------------------------ callers of the hot path ----
+def rho_k_all(points, k: int, config: BfConfig = None) -> np.ndarray:
+    """entropy.cpp:75-89: distance from every point to its k-th nearest other
+    point (self excluded by index), one device self-join + epilogue."""
+    P = _as_points(points)
+    n, d = P.shape
+    out = np.empty(n, np.float64)
+    o = _opts(config)
+    _check(library().knn_b200_rho_k_all(P.ctypes.data, n, d, int(k), C.byref(o), out.ctypes.data))
+    return out
+
+
+def rho_k_all_device(points_ptr: int, n: int, d: int, k: int, out_ptr: int,
+                     stream: int = 0) -> None:
+    """Device pointers: float32 n x d points in, float64 n distances out."""
+    o = _opts(stream=stream)
+    _check(library().knn_b200_rho_k_all_device(points_ptr, n, d, int(k), C.byref(o), out_ptr))
+
+
+def knn_classify(train_points, labels, queries, k: int, metric: Metric = None,
+                 config: BfConfig = None) -> np.ndarray:
+    """applications.cpp:36-63 (LabeledSet = train_points + labels)."""
+    T = _as_points(train_points)
+    Q = _as_points(queries)
+    lab = np.ascontiguousarray(labels, np.int64)
+    if lab.size != T.shape[0]:
+        raise ValueError(f"LabeledSet: {lab.size} labels for {T.shape[0]} points")
+    metric = metric or Metric.euclidean()
+    if metric.kind == MAHALANOBIS:
+        raise ValueError("knn_classify: use bf_knn for the Mahalanobis metric")
+    out = np.empty(Q.shape[0], np.int64)
+    o = _opts(config)
+    _check(library().knn_b200_knn_classify(T.ctypes.data, T.shape[0], T.shape[1], lab.ctypes.data,
+                                           Q.ctypes.data, Q.shape[0], Q.shape[1], int(k),
+                                           metric.kind, C.byref(o), out.ctypes.data))
+    return out
+
+
+@dataclass
+class VoteTally:
+    """applications.hpp: per-image vote counts and the ranking."""
+    scores: np.ndarray
+    ranking: np.ndarray
+
+
+def retrieve_vote(descriptors, image_of, image_count: int, query_descriptors, k: int,
+                  metric: Metric = None, config: BfConfig = None) -> VoteTally:
+    """applications.cpp:65-86 (DescriptorDatabase = descriptors + image_of)."""
+    D = _as_points(descriptors)
+    Q = _as_points(query_descriptors)
+    own = np.ascontiguousarray(image_of, np.int64)
+    if own.size != D.shape[0]:
+        raise ValueError(f"DescriptorDatabase: {own.size} owners for {D.shape[0]} descriptors")
+    metric = metric or Metric.euclidean()
+    if metric.kind == MAHALANOBIS:
+        raise ValueError("retrieve_vote: use bf_knn for the Mahalanobis metric")
+    ic = int(image_count)
+    scores = np.empty(max(ic, 1), np.uint64)
+    ranking = np.empty(max(ic, 1), np.int64)
+    o = _opts(config)
+    _check(library().knn_b200_retrieve_vote(D.ctypes.data, D.shape[0], D.shape[1], own.ctypes.data,
+                                            ic, Q.ctypes.data, Q.shape[0], Q.shape[1], int(k),
+                                            metric.kind, C.byref(o), scores.ctypes.data,
+                                            ranking.ctypes.data))
+    return VoteTally(scores[:ic], ranking[:ic])

@@ -97,4 +97,9 @@ void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int
 
 SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path);
 
+// PointSet's value check (point_set.hpp:27-31) on device rows: throws
+// InvalidArgument naming the first non-finite coordinate (capi.cu).
+void check_finite_device(cudaStream_t s, const float* X, int64_t rows, int64_t d,
+                         unsigned long long* dbad);
+
 }  // namespace knnb200
