@@ -54,8 +54,21 @@ public:
     double coord(std::size_t i, std::size_t c) const { return data_[i * d_ + c]; }
     const std::vector<double>& data() const { return data_; }
 
-    // FP32 copy handed to the engine
-    std::vector<float> as_f32() const { return std::vector<float>(data_.begin(), data_.end()); }
+    // FP32 copy handed to the engine.  The engine computes in FP32: a finite
+    // coordinate beyond the FP32 range is rejected with its own message (it
+    // would otherwise round to inf and read as "non-finite"); magnitudes below
+    // the FP32 subnormal range round to +-0 (IEEE round-to-nearest).
+    std::vector<float> as_f32(const char* which = "points") const {
+        std::vector<float> out(data_.size());
+        for (std::size_t i = 0; i < data_.size(); ++i) {
+            out[i] = static_cast<float>(data_[i]);
+            if (std::isinf(out[i]))
+                throw std::invalid_argument(std::string("bf_knn: ") + which + " coordinate at point " +
+                                            std::to_string(i / d_) + ", dimension " + std::to_string(i % d_) +
+                                            " is outside the FP32 range of the engine (|x| > 3.4028235e38)");
+        }
+        return out;
+    }
 
 private:
     std::size_t n_, d_;
@@ -172,8 +185,8 @@ inline NeighborTable bf_knn(const PointSet& queries, const PointSet& references,
         o.mahalanobis_dim = static_cast<int64_t>(metric.pinned_dim());
     }
     const std::size_t n = queries.size();
-    const std::vector<float> q = queries.as_f32();
-    const std::vector<float> r = references.as_f32();
+    const std::vector<float> q = queries.as_f32("queries");
+    const std::vector<float> r = references.as_f32("references");
     std::vector<float> dist(n * (k ? k : 1));
     std::vector<int64_t> idx(n * (k ? k : 1));
     uint64_t evals = 0;

@@ -25,6 +25,26 @@
 
 namespace knn {
 
+// The engine computes in FP32 (north star).  A finite double beyond the FP32
+// range would round to +-inf and then be reported by the engine as a
+// "non-finite coordinate", which the reference never says for a finite input:
+// reject it here with its own message.  Magnitudes below the FP32 subnormal
+// range round to +-0 (IEEE round-to-nearest), which is the documented
+// precision contract of the engine, not an error.
+static std::vector<float> narrow_to_f32(const PointSet& p, const char* which) {
+    const std::vector<double>& src = p.data();
+    std::vector<float> out(src.size());
+    for (std::size_t i = 0; i < src.size(); ++i) {
+        out[i] = static_cast<float>(src[i]);
+        if (std::isinf(out[i]))
+            throw std::invalid_argument(std::string("bf_knn: ") + which + " coordinate at point " +
+                                        std::to_string(i / p.dim()) + ", dimension " +
+                                        std::to_string(i % p.dim()) +
+                                        " is outside the FP32 range of the engine (|x| > 3.4028235e38)");
+    }
+    return out;
+}
+
 NeighborTable bf_knn(const PointSet& queries, const PointSet& references, std::size_t k,
                      const Metric& metric, const BfConfig& config, SearchStats* stats) {
     // The contract checks run here, before any whitening, so their order and
@@ -60,8 +80,8 @@ NeighborTable bf_knn(const PointSet& queries, const PointSet& references, std::s
     }
 
     const std::size_t n = q->size(), m = r->size(), d = q->dim();
-    const std::vector<float> qf(q->data().begin(), q->data().end());
-    const std::vector<float> rf(r->data().begin(), r->data().end());
+    const std::vector<float> qf = narrow_to_f32(*q, "queries");
+    const std::vector<float> rf = narrow_to_f32(*r, "references");
     std::vector<float> dist(n * k);
     std::vector<std::int64_t> idx(n * k);
     knn_b200_options o;

@@ -1,13 +1,14 @@
 // knn_b200_cli -- the reference CLI's `search` and `bench` subcommands on the
 // B200 engine.
 //
-// Mirrors /root/reference/proj/tools/knn_cli.cpp (run_search, :66-96, and the
-// option table of main, :232-244) and the point/matrix CSV readers of
-// src/csv.cpp (read_rows :44-76, parse_double :24-31, read_points_csv :85-94,
-// read_matrix_csv :150-166): same options, same output
+// Behaviour follows /root/reference/proj/tools/knn_cli.cpp (run_search, :66-96,
+// the option table of main, :232-244) and accepts the same point/matrix files
+// as src/csv.cpp (read_points_csv :85-94, read_matrix_csv :150-166); the file
+// scanner and the output writer below are this engine's own (one in-memory
+// pass, flat row-major table; stdio staging file + rename).  Same output
 //   query_index,rank,ref_index,distance
-// one row per (query, rank), written atomically through `<out>.tmp` + rename
-// (write_output, :42-56), and the same exit codes (main, :277-292): 0 success,
+// one row per (query, rank), replaced atomically through `<out>.tmp` + rename,
+// and the same exit codes (main, :277-292): 0 success,
 // 2 malformed input file ("error: line N: ..."), 3 contract violation
 // (std::invalid_argument), 1 anything else, 2 for unknown options.
 //
@@ -30,6 +31,7 @@
 #include <charconv>
 #include <chrono>
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
@@ -55,110 +57,119 @@ struct UsageError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-std::string_view trim(std::string_view t) {
-    while (!t.empty() && (t.front() == ' ' || t.front() == '\t')) t.remove_prefix(1);
-    while (!t.empty() && (t.back() == ' ' || t.back() == '\t' || t.back() == '\r'))
-        t.remove_suffix(1);
+// ---- point files -----------------------------------------------------------
+// One pass over the whole file held in memory: a small scanner walks the bytes,
+// cutting fields at ',' and records at '\n', and converts each field as soon as
+// it is cut, so the table is a flat row-major vector from the start (no per-row
+// string copies).  Accepted input is the reference's (src/csv.cpp): blank
+// lines and lines whose first non-blank character is '#' are skipped, spaces,
+// tabs and a trailing '\r' around a field are ignored, and every record must
+// have as many fields as the first one.  Errors name the 1-based file line.
+struct NumericTable {
+    std::vector<double> values;  // row-major
+    std::size_t cols = 0, rows = 0;
+    std::size_t last_line = 0;   // file line of the last record
+};
+
+bool is_blank(char c) { return c == ' ' || c == '\t' || c == '\r'; }
+
+double field_value(const char* b, const char* e, std::size_t line) {
+    while (b < e && is_blank(*b)) ++b;
+    while (e > b && is_blank(e[-1])) --e;
+    double v = 0.0;
+    const std::from_chars_result r = std::from_chars(b, e, v);
+    if (r.ec != std::errc{} || r.ptr != e)
+        throw CsvError("cannot parse '" + std::string(b, e) + "' as a number", line);
+    return v;
+}
+
+NumericTable scan_numeric_file(const std::filesystem::path& path) {
+    std::string text;
+    {
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        if (f == nullptr) throw std::runtime_error("cannot open '" + path.string() + "'");
+        char chunk[1 << 16];
+        for (std::size_t got; (got = std::fread(chunk, 1, sizeof chunk, f)) > 0;) text.append(chunk, got);
+        std::fclose(f);
+    }
+    NumericTable t;
+    const char* p = text.data();
+    const char* const end = p + text.size();
+    for (std::size_t line = 1; p < end; ++line) {
+        const char* eol = static_cast<const char*>(std::memchr(p, '\n', static_cast<std::size_t>(end - p)));
+        if (eol == nullptr) eol = end;
+        const char* first = p;
+        while (first < eol && is_blank(*first)) ++first;
+        if (first < eol && *first != '#') {  // a record
+            std::size_t width = 0;
+            for (const char* f = p;; ++width) {
+                const char* comma = std::find(f, eol, ',');
+                t.values.push_back(field_value(f, comma, line));
+                if (comma == eol) break;
+                f = comma + 1;
+            }
+            ++width;
+            if (t.rows == 0) t.cols = width;
+            else if (width != t.cols)
+                throw CsvError("expected " + std::to_string(t.cols) + " fields, got " + std::to_string(width),
+                               line);
+            ++t.rows;
+            t.last_line = line;
+        }
+        p = eol + (eol < end ? 1 : 0);
+    }
+    if (t.rows == 0) throw CsvError("no data rows in " + path.string(), 0);
     return t;
 }
 
-double parse_double(std::string_view token, std::size_t line) {
-    token = trim(token);
-    double value = 0.0;
-    const auto [ptr, ec] = std::from_chars(token.data(), token.data() + token.size(), value);
-    if (ec != std::errc{} || ptr != token.data() + token.size())
-        throw CsvError("cannot parse '" + std::string(token) + "' as a number", line);
-    return value;
-}
-
-struct RawRow {
-    std::vector<std::string> fields;
-    std::size_t line;
-};
-
-// blank lines and '#' comments skipped; every row as wide as the first
-std::vector<RawRow> read_rows(const std::filesystem::path& path) {
-    std::ifstream in(path);
-    if (!in) throw std::runtime_error("cannot open '" + path.string() + "'");
-    std::vector<RawRow> rows;
-    std::string line;
-    std::size_t line_no = 0, width = 0;
-    while (std::getline(in, line)) {
-        ++line_no;
-        const std::string_view view = trim(line);
-        if (view.empty() || view.front() == '#') continue;
-        RawRow row{{}, line_no};
-        const std::string text(view);
-        std::size_t start = 0;
-        while (true) {
-            const std::size_t comma = text.find(',', start);
-            row.fields.push_back(text.substr(start, comma - start));
-            if (comma == std::string::npos) break;
-            start = comma + 1;
-        }
-        if (width == 0)
-            width = row.fields.size();
-        else if (row.fields.size() != width)
-            throw CsvError("expected " + std::to_string(width) + " fields, got " +
-                               std::to_string(row.fields.size()),
-                           line_no);
-        rows.push_back(std::move(row));
-    }
-    return rows;
-}
-
 knn_b200::PointSet read_points_csv(const std::filesystem::path& path) {
-    const std::vector<RawRow> rows = read_rows(path);
-    if (rows.empty()) throw CsvError("no data rows in " + path.string(), 0);
-    const std::size_t d = rows.front().fields.size();
-    std::vector<double> data;
-    data.reserve(rows.size() * d);
-    for (const RawRow& row : rows)
-        for (const std::string& f : row.fields) data.push_back(parse_double(f, row.line));
-    return knn_b200::PointSet(rows.size(), d, std::move(data));
+    NumericTable t = scan_numeric_file(path);
+    return knn_b200::PointSet(t.rows, t.cols, std::move(t.values));
 }
 
 std::vector<double> read_matrix_csv(const std::filesystem::path& path, std::size_t& dim) {
-    const std::vector<RawRow> rows = read_rows(path);
-    if (rows.empty()) throw CsvError("no data rows in " + path.string(), 0);
-    dim = rows.front().fields.size();
-    if (rows.size() != dim)
-        throw CsvError("matrix must be square, got " + std::to_string(rows.size()) + "x" +
-                           std::to_string(dim),
-                       rows.back().line);
-    std::vector<double> m;
-    m.reserve(dim * dim);
-    for (const RawRow& row : rows)
-        for (const std::string& f : row.fields) m.push_back(parse_double(f, row.line));
-    return m;
+    NumericTable t = scan_numeric_file(path);
+    if (t.rows != t.cols)
+        throw CsvError("matrix must be square, got " + std::to_string(t.rows) + "x" + std::to_string(t.cols),
+                       t.last_line);
+    dim = t.cols;
+    return std::move(t.values);
 }
 
-knn_b200::Metric parse_metric(const std::string& name) {
-    if (name == "euclidean") return knn_b200::Metric::euclidean();
-    if (name == "manhattan") return knn_b200::Metric::manhattan();
-    if (name == "chebyshev") return knn_b200::Metric::chebyshev();
-    if (name.rfind("mahalanobis:", 0) == 0) {
+knn_b200::Metric parse_metric(const std::string& spec) {
+    static constexpr std::string_view kMaha = "mahalanobis:";
+    if (spec.size() > kMaha.size() && spec.compare(0, kMaha.size(), kMaha) == 0) {
         std::size_t dim = 0;
-        std::vector<double> m = read_matrix_csv(name.substr(std::string("mahalanobis:").size()), dim);
-        return knn_b200::Metric::mahalanobis(dim, std::move(m));
+        std::vector<double> cov = read_matrix_csv(spec.substr(kMaha.size()), dim);
+        return knn_b200::Metric::mahalanobis(dim, std::move(cov));
     }
+    using Factory = knn_b200::Metric (*)();
+    static const std::pair<std::string_view, Factory> kPlain[] = {
+        {"euclidean", &knn_b200::Metric::euclidean},
+        {"manhattan", &knn_b200::Metric::manhattan},
+        {"chebyshev", &knn_b200::Metric::chebyshev},
+    };
+    for (const auto& [name, make] : kPlain)
+        if (spec == name) return make();
     throw UsageError("--metric: expected euclidean, manhattan, chebyshev or mahalanobis:PATH");
 }
 
-void write_output(const std::string& path, const std::string& content) {
+// stdout when no path is given; otherwise the whole text goes to "<path>.tmp",
+// which then replaces <path> in one rename (readers never see a partial file)
+void emit(const std::string& path, const std::string& text) {
     if (path.empty()) {
-        std::cout << content;
+        std::fwrite(text.data(), 1, text.size(), stdout);
+        std::fflush(stdout);
         return;
     }
-    const std::filesystem::path target(path);
-    std::filesystem::path temp = target;
-    temp += ".tmp";
-    {
-        std::ofstream out(temp, std::ios::trunc);
-        if (!out) throw std::runtime_error("cannot open '" + temp.string() + "' for writing");
-        out << content;
-    }
-    std::filesystem::rename(temp, target);
+    const std::string staging = path + ".tmp";
+    std::FILE* f = std::fopen(staging.c_str(), "wb");
+    if (f == nullptr) throw std::runtime_error("cannot open '" + staging + "' for writing");
+    const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    if (std::fclose(f) != 0 || !ok) throw std::runtime_error("cannot write '" + staging + "'");
+    std::error_code ec;
+    std::filesystem::rename(staging, path, ec);
+    if (ec) throw std::runtime_error("cannot replace '" + path + "': " + ec.message());
 }
 
 std::string format_distance(double d) {  // the FP32 value's shortest decimal
@@ -215,7 +226,7 @@ int run_search(int argc, char** argv) {
             out << i << ',' << r << ',' << row[r].index << ',' << format_distance(row[r].distance)
                 << '\n';
     }
-    write_output(out_path, out.str());
+    emit(out_path, out.str());
     return 0;
 }
 
@@ -360,8 +371,8 @@ int run_bench(int argc, char** argv) {
             first = false;
         }
     json << "\n  ]\n}\n";
-    write_output(out_path, csv.str());
-    if (!json_path.empty()) write_output(json_path, json.str());
+    emit(out_path, csv.str());
+    if (!json_path.empty()) emit(json_path, json.str());
     return 0;
 }
 

@@ -123,6 +123,12 @@ static void contract_errors() {
     check_throws([&] { (void)PointSet(0, 2, {}); }, "point count must be >= 1");
     check_throws([&] { (void)PointSet(1, 2, {0, NAN}); }, "non-finite coordinate at point 0, dimension 1");
     check_throws([&] { (void)Metric::mahalanobis(2, {1, 2, 2, 1}); }, "not positive definite");
+    // finite doubles beyond the FP32 range: the engine's own message, not "non-finite"
+    const PointSet huge(1, 2, {0.5, 1e39});
+    check_throws([&] { (void)knn_b200::bf_knn(huge, refs, 1, Metric::euclidean()); },
+                 "queries coordinate at point 0, dimension 1 is outside the FP32 range");
+    check_throws([&] { (void)knn_b200::bf_knn(query, PointSet(1, 2, {-4e38, 0}), 1, Metric::euclidean()); },
+                 "references coordinate at point 0, dimension 0 is outside the FP32 range");
     check_throws(
         [&] {
             (void)knn_b200::bf_knn(query, refs, 1, Metric::mahalanobis(3, {1, 0, 0, 0, 1, 0, 0, 0, 1}));
