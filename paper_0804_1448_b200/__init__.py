@@ -31,6 +31,8 @@ __all__ = [
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libknn_b200.so")
+# dev-only: A/B builds of the same library (tools/build_variant.sh)
+lib_path = os.environ.get("_KNN_B200_DEV_LIB", lib_path)
 
 EUCLIDEAN, MANHATTAN, CHEBYSHEV, MAHALANOBIS = 0, 1, 2, 3
 PATH_AUTO, PATH_EXACT, PATH_TENSOR = 0, 1, 2

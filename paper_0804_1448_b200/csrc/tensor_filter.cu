@@ -16,6 +16,15 @@ namespace tp {
 
 namespace {
 
+// Dev-only filter modes (KNN_B200_FILTER_MODE: 2 no epilogue work, 3 no pushes,
+// used to measure floors); compiled out of the product build, where the hot
+// loop carries no mode checks.
+#ifdef KNN_B200_DEV_MODES
+__device__ __forceinline__ int kMode(const FilterArgs& a) { return a.mode; }
+#else
+__device__ __forceinline__ constexpr int kMode(const FilterArgs&) { return 0; }
+#endif
+
 // Persistent tcgen05 filter.  A work unit is one 128-reference tile against a
 // resident PAIR of 128-query tiles: warp 0 streams reference tiles by TMA;
 // one thread of warp 1 (query tile 0) and one of warp 3 (query tile 1) issue
@@ -26,7 +35,7 @@ namespace {
 // flight ahead of the scan).  Each query keeps one bound list per CTA part;
 // pushed groups go to the global group log, their minima to a shared-memory
 // buffer that the drain inserts into the list once per tile.
-template <int KR>
+template <int KR, bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
                   FilterArgs a) {
@@ -151,14 +160,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     do {                                                                                         \
         float v_[32];                                                                            \
         _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
-        if (!a.fold) add_rnorm_smem(v_, rnw + ((colb) - col_base));                              \
+        if (!FOLD) add_rnorm_smem(v_, rnw + ((colb) - col_base));                              \
         float gm_[4];                                                                            \
         _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_) {                                       \
             const float* w_ = v_ + 8 * i_;                                                       \
             gm_[i_] = fminf(min3(min3(w_[0], w_[1], w_[2]), min3(w_[3], w_[4], w_[5]), w_[6]),   \
                             w_[7]);                                                              \
         }                                                                                        \
-        if (a.mode != 3 &&                                                                       \
+        if (kMode(a) != 3 &&                                                                       \
             __any_sync(0xffffffffu, fminf(fminf(gm_[0], gm_[1]), fminf(gm_[2], gm_[3])) <= tfp)) { \
             _Pragma("unroll") for (int i_ = 0; i_ < 4; ++i_)                                     \
                 push_group<EPI_THREADS * 4>(gm_[i_], tfp, sgp, ln, lvb, lhb, v_ + 8 * i_,        \
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // (tcgen05.wait::ld waits for all): the load of chunk c+1 -- chunk 0
         // of the next tile after chunk 3 -- overlaps the scan of chunk c.
         uint32_t ra[32], rb[32];
-        if (a.mode != 2 && nunits > 0) {
+        if (kMode(a) != 2 && nunits > 0) {
             wait_full(0);
             sm100::tmem_ld_32x32b_x32(tlane, ra);
             sm100::tmem_ld_wait();
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // read back as broadcasts, instead of 8 global loads per chunk
         float* const rnw = RN + ew * TILE;
         float4 rn_nx = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!a.fold && nunits > 0)
+        if (!FOLD && nunits > 0)
             rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + rt * TILE) + lane);
         for (int t = 0; t < nunits; ++t) {
             if (p != cur_p) {
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             tfp = ln > a.CG - 16 ? -kInf : Tf;
             const int col_base = rt * TILE;
             const uint32_t taddr = tlane + static_cast<uint32_t>((t & 1) * TILE);
-            if (!a.fold) {  // stage this unit's norms, prefetch the next unit's
+            if (!FOLD) {  // stage this unit's norms, prefetch the next unit's
                 __syncwarp();
                 reinterpret_cast<float4*>(rnw)[lane] = rn_nx;
                 __syncwarp();
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + nrt * TILE) + lane);
                 }
             }
-            if (a.mode == 2) {
+            if (kMode(a) == 2) {
                 wait_full(t);
                 release(t);
             } else {
@@ -483,15 +492,18 @@ void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const F
         ProfileScope ps(stream, "tc_filter_kernel");
         KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
     };
+#define KNN_F(KRV) \
+    if (fa.fold) go(filter_kernel<KRV, true>); else go(filter_kernel<KRV, false>)
     switch (Kq) {
-        case 4: go(filter_kernel<4>); break;
-        case 8: go(filter_kernel<8>); break;
-        case 12: go(filter_kernel<12>); break;
-        case 16: go(filter_kernel<16>); break;
-        case 20: go(filter_kernel<20>); break;
-        case 24: go(filter_kernel<24>); break;
-        default: go(filter_kernel<32>); break;
+        case 4: KNN_F(4); break;
+        case 8: KNN_F(8); break;
+        case 12: KNN_F(12); break;
+        case 16: KNN_F(16); break;
+        case 20: KNN_F(20); break;
+        case 24: KNN_F(24); break;
+        default: KNN_F(32); break;
     }
+#undef KNN_F
     KNN_LAUNCH_CHECK();
 }
 

@@ -1,7 +1,9 @@
 """Dev tool (GPU): per-kernel device times of the tensor path on one shape,
 optionally under the filter kernel's dev modes (KNN_B200_FILTER_MODE:
 0 full, 1 TMEM load + min only, 2 no epilogue work).  Results are only
-meaningful for mode 0; the other modes measure floors.
+meaningful for mode 0; the other modes measure floors and need the dev build
+(bash tools/build_variant.sh devmodes -DKNN_B200_DEV_MODES, then run with
+_KNN_B200_DEV_LIB=build_variants/devmodes/libknn_b200.so).
 
     python tools/filter_modes.py [n m d k] [reps]
 """
