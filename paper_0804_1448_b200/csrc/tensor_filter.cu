@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }                                                                                        \
         sgp = sg0;                                                                               \
         if (L.cnt >= k) {                                                                        \
-            const float tn_ = thresh(L.kth(k), qc);                                              \
+            const float tn_ = thresh(k == KR ? L.key[KR - 1] : L.kth(k), qc);                    \
             if (tn_ < T) {                                                                       \
                 T = tn_;                                                                         \
                 atomicMin(a.tglob + q, enc(T));                                                  \

@@ -177,8 +177,9 @@ template <int STRIDE>
 __device__ __forceinline__ void push_group(float gm, float tf, uint32_t& sgp, int& off, float4* lvb,
                                            int2* lhb, const float* w, int col) {
     const bool hit = gm <= tf;
-    float4* pv = lvb + 2 * off;
-    int2* ph = lhb + off;
+    // byte offsets from the per-lane bases: one wide multiply-add per address
+    float4* pv = reinterpret_cast<float4*>(reinterpret_cast<char*>(lvb) + static_cast<uint64_t>(static_cast<uint32_t>(off)) * 32u);
+    int2* ph = reinterpret_cast<int2*>(reinterpret_cast<char*>(lhb) + static_cast<uint64_t>(static_cast<uint32_t>(off)) * 8u);
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %0, 0;\n\t"

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "profile.cuh"
@@ -215,6 +217,148 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
     }
 }
 
+// Row-quad layout of the same conversion for d % 4 == 0 (every configuration
+// of the benchmark): 4 lanes per row, 8 rows per warp.  Lane l of a row owns
+// the 4-coordinate granules g = l, l + 4, ..., loads them with 128-bit loads
+// (the 4 lanes of a row read 64 contiguous bytes per instruction), writes
+// their fp16 images with 64-bit stores (32 contiguous bytes per row), and the
+// per-row sums reduce over the 4 lanes (2 shuffle levels instead of 5).  The
+// arithmetic per coordinate is convert_kernel's, so Xh, the norms and the
+// radii agree with it up to the (exact-double) summation order.
+template <bool QUERY, int GPL>  // GPL: granules per lane (d <= 16 GPL)
+__global__ void __launch_bounds__(256) convert4_kernel(PrepArgs a) {
+    if (QUERY) sm100::pdl_trigger();
+    __shared__ float red[2][8];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int l4 = lane & 3;
+    const float s = *a.scale;
+    if (QUERY && a.zero && blockIdx.x == 0 && threadIdx.x == 0) *a.zero = 0;
+    if (QUERY && a.pair_slots)
+        for (int p = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x); p < a.pairs;
+             p += static_cast<int>(gridDim.x * blockDim.x)) {
+            const int64_t u0 = static_cast<int64_t>(p) * a.rtiles;
+            a.pair_slots[p] = first_cta_of(u0 + a.rtiles - 1, a.U, a.G) - first_cta_of(u0, a.U, a.G) + 1;
+        }
+    const int ng = a.d >> 2;       // coordinate granules
+    const int nk = a.Kp >> 2;      // output granules (4 halves each)
+    float dmax = 0.f, nmax = 0.f;
+    const int64_t rstep = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 2);
+    for (int64_t row0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 2); row0 < a.rows_pad;
+         row0 += rstep) {
+        const int64_t row = row0 + (threadIdx.x >> 2);
+        const bool inpad = row < a.rows_pad;
+        const bool real = row < a.rows;
+        float4 x[GPL];
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+            const int g = 4 * j + l4;
+            x[j] = (real && g < ng) ? __ldg(reinterpret_cast<const float4*>(a.X + row * a.d) + g)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        double h2 = 0.0, e2 = 0.0;
+        bool ovf = false;
+        uint2* out = reinterpret_cast<uint2*>(a.Xh + row * a.Kp);
+#pragma unroll
+        for (int j = 0; j < GPL; ++j) {
+            const int g = 4 * j + l4;
+            if (g < ng) {
+                const float xc[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+                __half hq[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __half h = __float2half_rn(0.f);
+                    if (real) {
+                        const float t = __fsub_rn(xc[e], a.mu[4 * g + e]) * s;
+                        h = __float2half_rn(t);
+                        const double hv = static_cast<double>(__half2float(h));
+                        const double err = fabs(hv - static_cast<double>(t)) + fabs(static_cast<double>(t)) * 0x1.0p-23;
+                        h2 += hv * hv;
+                        e2 += err * err;
+                        if (QUERY) {
+                            h = __float2half_rn(-2.f * __half2float(h));
+                            ovf |= __hisinf(h) != 0;
+                        }
+                    }
+                    hq[e] = h;
+                }
+                if (inpad) {
+                    uint2 w;
+                    w.x = static_cast<uint32_t>(__half_as_ushort(hq[0])) | (static_cast<uint32_t>(__half_as_ushort(hq[1])) << 16);
+                    w.y = static_cast<uint32_t>(__half_as_ushort(hq[2])) | (static_cast<uint32_t>(__half_as_ushort(hq[3])) << 16);
+                    out[g] = w;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        }
+        const bool any_ovf = (__ballot_sync(0xffffffffu, ovf) >> (lane & ~3) & 0xfu) != 0;
+        const float delta = any_ovf ? kInf : static_cast<float>(sqrt(e2) * (1.0 + 0x1.0p-20)) * (1.f + 1e-6f);
+        const float xn = static_cast<float>(sqrt(h2)) * (1.f + 1e-6f);
+        // tail columns [d, Kp): zeros, or the three folded-norm columns
+        __half nc[3];
+        if (QUERY) {
+            nc[0] = nc[1] = nc[2] = __float2half_rn(1.f);
+        } else if (real) {
+            nc[0] = __double2half(h2);
+            const double r1 = h2 - static_cast<double>(__half2float(nc[0]));
+            nc[1] = __double2half(r1);
+            nc[2] = __double2half(r1 - static_cast<double>(__half2float(nc[1])));
+        } else {
+            nc[0] = __float2half_rn(kInf);  // padding: A = +inf
+            nc[1] = nc[2] = __float2half_rn(0.f);
+        }
+        if (inpad)
+            for (int g = ng + l4; g < nk; g += 4) {
+                unsigned short hv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int c = 4 * g + e;
+                    const int nci = c - a.norm_col;
+                    hv[e] = (a.norm_col >= 0 && nci >= 0 && nci < 3) ? __half_as_ushort(nc[nci]) : 0;
+                }
+                out[g] = make_uint2(hv[0] | (static_cast<uint32_t>(hv[1]) << 16),
+                                    hv[2] | (static_cast<uint32_t>(hv[3]) << 16));
+            }
+        if (inpad && l4 == 0) {
+            if (QUERY) {
+                a.qconst[row] = make_float4(static_cast<float>(h2), delta, xn, 0.f);
+                if (a.tinit) a.tinit[row] = 0xffffffffu;
+            } else if (a.norm_col < 0) {
+                a.norm[row] = real ? static_cast<float>(h2) : kInf;
+            }
+        }
+        if (!QUERY && real) {
+            dmax = fmaxf(dmax, delta);
+            nmax = fmaxf(nmax, xn);
+        }
+    }
+    if (!QUERY) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+            nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        }
+        if (lane == 0) {
+            red[0][wib] = dmax;
+            red[1][wib] = nmax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float dm = 0.f, nm = 0.f;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+                dm = fmaxf(dm, red[0][w]);
+                nm = fmaxf(nm, red[1][w]);
+            }
+            atomicMax(a.gmax + 0, __float_as_uint(dm));
+            atomicMax(a.gmax + 1, __float_as_uint(nm));
+        }
+    }
+}
+
 }  // namespace
 
 void launch_range(const float* X, int64_t rows, int d, unsigned* mn, unsigned* mx,
@@ -242,6 +386,26 @@ void launch_scale(const unsigned* mn, const unsigned* mx, int d, int Kp, float* 
 }
 
 void launch_convert(const PrepArgs& pr, bool query, cudaStream_t stream) {
+    if (pr.d % 4 == 0 && pr.d <= 128 && std::getenv("KNN_B200_CONVERT_V1") == nullptr) {
+        // 64 rows per block step; enough blocks to fill the SMs several times over
+        const unsigned grid =
+            static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((pr.rows_pad + 63) / 64, 16 * kSmCount)));
+        const int gpl = (pr.d / 4 + 3) / 4;
+        ProfileScope ps(stream, query ? "prep_convert_queries" : "prep_convert_refs");
+        auto go = [&](auto kq, auto kr) {
+            (void)kq;
+            (void)kr;
+            convert4_kernel<decltype(kq)::value, decltype(kr)::value><<<grid, 256, 0, stream>>>(pr);
+        };
+        using T = std::true_type;
+        using F = std::false_type;
+        if (gpl <= 2) query ? go(T{}, std::integral_constant<int, 2>{}) : go(F{}, std::integral_constant<int, 2>{});
+        else if (gpl <= 4) query ? go(T{}, std::integral_constant<int, 4>{}) : go(F{}, std::integral_constant<int, 4>{});
+        else if (gpl <= 6) query ? go(T{}, std::integral_constant<int, 6>{}) : go(F{}, std::integral_constant<int, 6>{});
+        else query ? go(T{}, std::integral_constant<int, 8>{}) : go(F{}, std::integral_constant<int, 8>{});
+        KNN_LAUNCH_CHECK();
+        return;
+    }
     const unsigned grid =
         static_cast<unsigned>(std::min<int64_t>((pr.rows_pad + 7) / 8, 8 * kSmCount));
     {
