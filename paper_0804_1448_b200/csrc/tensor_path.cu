@@ -125,6 +125,8 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     const int64_t m_pad = static_cast<int64_t>(rtiles) * TILE;
     const int64_t U = static_cast<int64_t>(pairs) * rtiles;
     const bool large = k > MAX_KQ;
+    if (large && !retry)
+        if (const char* e = std::getenv("KNN_B200_LARGE_MARGIN")) margin = std::max(1, std::atoi(e));  // dev
     // at most ~29 CTAs share a query-tile pair, so a query has <= 32 partial lists
     const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
                                                      static_cast<int64_t>(pairs) * 29));

@@ -200,6 +200,31 @@ __device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist
     return dec(prefix);
 }
 
+// Block-wide exclusive prefix sum of one int per thread (NT threads); the
+// block total in *total.  Contains barriers: every thread must call it.
+template <int NT>
+__device__ int block_exclusive_scan(int v, int* total) {
+    __shared__ int s_w[NT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();  // s_w of a previous call has been read
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    int base = incl - v, tot = 0;
+#pragma unroll
+    for (int x = 0; x < NT / 32; ++x) {
+        base += x < w ? s_w[x] : 0;
+        tot += s_w[x];
+    }
+    *total = tot;
+    return base;
+}
+
 // NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
 // capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
 template <int NT>
@@ -254,18 +279,18 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
         tau = thresh(ak, qc);
         ok = tau <= T0;  // every reference with A <= tau was logged
         if (ok) {
-            // compact the candidates (A <= tau) to the front, any order
-            if (threadIdx.x == 0) s_cnt = 0;
-            __syncthreads();
-            int mine[16];  // total <= NC <= 16 * NT: a thread owns <= 16 entries
+            // compact the candidates (A <= tau) to the front in log order, i.e.
+            // ascending reference index (parts in slot order, each part's log in
+            // stream order); thread t owns the contiguous range [t per, t per + per)
+            const int per = (total + NT - 1) / NT;  // <= NC / NT <= 16
+            const int e0 = min(total, static_cast<int>(threadIdx.x) * per), e1 = min(total, e0 + per);
+            int mine[16];
             int nm = 0;
-            for (int e = threadIdx.x; e < total; e += blockDim.x)
+            for (int e = e0; e < e1; ++e)
                 if (sk[e] <= tau) mine[nm++] = si[e];
-            __syncthreads();
-            const int base = atomicAdd(&s_cnt, nm);
+            const int base = block_exclusive_scan<NT>(nm, &nc);
             for (int j = 0; j < nm; ++j) si[base + j] = mine[j];
             __syncthreads();
-            nc = s_cnt;
         }
     }
     if (!ok) {
@@ -282,8 +307,50 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
     const float* qrow = a.Q + q * a.d;
     for (int c = threadIdx.x; c < nc; c += blockDim.x)
         sk[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(si[c]) * a.d, a.d);
-    int N2 = 32;
+    // Preselection: when the candidates need a longer network than k does,
+    // keep exactly the k smallest under the (key, index) order first -- every
+    // key below the k-th smallest K, then the lowest-index entries equal to K
+    // (the array is in ascending index order) -- so the bitonic network sorts
+    // k rounded up to a power of two (k = 1024: 1024 instead of 2048 entries
+    // for the ~1.1k candidates).
+    int N2 = 32, Nk = 32;
     while (N2 < nc) N2 <<= 1;
+    while (Nk < k) Nk <<= 1;
+    __syncthreads();
+    if (N2 > Nk) {
+        const float K = block_kth_smallest(sk, nc, k, s_hist, s_sel);
+        const int per = (nc + NT - 1) / NT;
+        const int e0 = min(nc, static_cast<int>(threadIdx.x) * per), e1 = min(nc, e0 + per);
+        int nl = 0, ne = 0;
+        for (int e = e0; e < e1; ++e) {
+            nl += sk[e] < K ? 1 : 0;
+            ne += sk[e] == K ? 1 : 0;
+        }
+        int tot_less = 0, tot_eq = 0;
+        block_exclusive_scan<NT>(nl, &tot_less);
+        const int eq_before = block_exclusive_scan<NT>(ne, &tot_eq);
+        const int need_eq = k - tot_less;  // >= 1 (K is the k-th smallest)
+        float mk[16];
+        int mi[16];
+        int nm = 0, eq_seen = eq_before;
+        for (int e = e0; e < e1; ++e) {
+            const float x = sk[e];
+            const bool keep = x < K || (x == K && eq_seen++ < need_eq);
+            if (keep) {
+                mk[nm] = x;
+                mi[nm] = si[e];
+                ++nm;
+            }
+        }
+        int kept = 0;
+        const int base = block_exclusive_scan<NT>(nm, &kept);  // kept == k
+        for (int j = 0; j < nm; ++j) {
+            sk[base + j] = mk[j];
+            si[base + j] = mi[j];
+        }
+        nc = kept;
+        N2 = Nk;
+    }
     for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
         sk[e] = kInf;
         si[e] = 0x7fffffff;
