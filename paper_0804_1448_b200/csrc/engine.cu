@@ -11,6 +11,7 @@
 //                exact re-rank -> exact fallback for uncertified queries)
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 
@@ -93,9 +94,11 @@ SearchPlan plan_search(int64_t n, int64_t m, int d, int k, int metric, int path)
     return p;
 }
 
-static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
-                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
-                      int64_t index_base, float* d_out, int64_t* d_idx) {
+// the list path of the exact kernel (any k): lists in shared memory up to
+// k = 128, global memory beyond
+void run_exact_lists(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                     const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                     int64_t index_base, float* d_out, int64_t* d_idx) {
     const bool big_k = static_cast<size_t>(k) > exact_smem_list_limit_k();
     ExactArgs a{};
     a.Q = dQ;
@@ -137,6 +140,24 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
         a.mglist_idx = cv.take<int64_t>(static_cast<size_t>(n) * k);
     }
     launch_exact(metric, a, stream);
+}
+
+// exact path: the threshold-log path for 128 < k <= 1024 on large reference
+// sets (exact_large.cu), the list path otherwise (dev knob
+// KNN_B200_EXACT_LARGE=0 forces the list path)
+static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                      int64_t index_base, float* d_out, int64_t* d_idx) {
+    static const bool large_ok = [] {
+        const char* e = std::getenv("KNN_B200_EXACT_LARGE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (large_ok && exact_large_applies(m, k)) {
+        run_exact_large(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);
+        ctx.s->fb_on_device = false;
+        return;
+    }
+    run_exact_lists(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);
 }
 
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,

@@ -90,6 +90,15 @@ struct TensorRefs;
 // Core device search.  All pointers are device pointers.  Output: finalized
 // distances (or raw keys when raw_keys) and global indices (index_base + j).
 // refs: the tensor path's prepared reference set (index handles), optional.
+// exact path pieces (engine.cu, exact_large.cu)
+void run_exact_lists(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                     const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                     int64_t index_base, float* d_out, int64_t* d_idx);
+bool exact_large_applies(int64_t m, int k);
+void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                     const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                     int64_t index_base, float* d_out, int64_t* d_idx);
+
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                    const float* dR, int64_t m, int d, int k, int metric, int path,
                    int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx,

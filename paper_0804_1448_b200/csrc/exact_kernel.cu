@@ -81,10 +81,15 @@ __device__ __forceinline__ float2 key_step2(float2 acc, float q, float2 r) {
 // lane (k <= 32 KP); KP < 0: lists in global memory, register bursts of -KP
 // (128 < k <= 256); 0: lists in global memory, WarpList (k > 256; larger
 // register bursts spill).
+// KP == kLogKP: threshold-log mode (exact_large.cu): no lists; every key at
+// or under the row's threshold t0 is appended to the segment's log.
+constexpr int kLogKP = 1000;
+
 template <int M, int KP, bool INDIRECT = false>
 __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
-    constexpr bool SMEM_LISTS = KP > 0;  // KP < 0: global lists, register bursts of -KP
-    constexpr int RP = KP > 0 ? KP : -KP;
+    constexpr bool LOG = KP == kLogKP;
+    constexpr bool SMEM_LISTS = KP > 0 && !LOG;  // KP < 0: global lists, register bursts of -KP
+    constexpr int RP = LOG ? 1 : (KP > 0 ? KP : -KP);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* stages = reinterpret_cast<float*>(smem_raw);      // [NSTAGE][STAGE]
     float* Lk = stages + NSTAGE * STAGE;                       // [QT][k] (smem lists)
@@ -101,7 +106,11 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
 
     const int d = a.d;
     const int64_t m = a.m;
-    if constexpr (!SMEM_LISTS) {
+    if constexpr (LOG) {  // per-row threshold and log length in shared memory
+        sc = reinterpret_cast<float*>(smem_raw) + NSTAGE * STAGE + (threadIdx.x >> 5) * 2 * RT;
+        Lk = reinterpret_cast<float*>(smem_raw) + NSTAGE * STAGE + (THREADS / 32) * 2 * RT;  // [QT] thresholds
+        Li = reinterpret_cast<int32_t*>(Lk + QT);                                          // [QT] log lengths
+    } else if constexpr (!SMEM_LISTS) {
         Lk = a.glist_key + static_cast<size_t>(blockIdx.x) * QT * a.k;
         Li = a.glist_idx + static_cast<size_t>(blockIdx.x) * QT * a.k;
     }
@@ -130,12 +139,21 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
         const size_t slot = static_cast<size_t>(blockIdx.x + b);
 
         // warp w owns rows 2w + h + 16 i (h < 2, i < 8): its 16 lists are private
-        for (int i = 0; i < 8; ++i)
-            for (int h = 0; h < 2; ++h) {
-                const int row = 2 * warp + h + 16 * i;
-                WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
-                L.init(lane);
+        if constexpr (LOG) {
+            if (lane < 16) {
+                const int row = 2 * warp + (lane & 1) + 16 * (lane >> 1);
+                const int64_t q = b * QT + row;
+                Lk[row] = q < n_eff ? a.t0[q * a.t0_stride] : -kInf;
+                Li[row] = 0;
             }
+        } else {
+            for (int i = 0; i < 8; ++i)
+                for (int h = 0; h < 2; ++h) {
+                    const int row = 2 * warp + h + 16 * i;
+                    WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
+                    L.init(lane);
+                }
+        }
         __syncwarp();
 
         // stage loader: Q rows q0.. (row-major, 32 coords) and R rows t0..
@@ -238,7 +256,8 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
                     float mn = fminf(acc[i][0].x, acc[i][0].y);
 #pragma unroll
                     for (int jp = 1; jp < 4; ++jp) mn = fminf(mn, fminf(acc[i][jp].x, acc[i][jp].y));
-                    const float thr = Lk[(2 * warp + half + 16 * i) * a.k + a.k - 1];
+                    const float thr = LOG ? Lk[2 * warp + half + 16 * i]
+                                          : Lk[(2 * warp + half + 16 * i) * a.k + a.k - 1];
                     const unsigned vote = __ballot_sync(0xffffffffu, mn <= thr);
                     if (vote == 0u) continue;
                     // stage the row pair's 2 x 128 keys in the warp's scratch
@@ -251,7 +270,25 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
                     for (int h = 0; h < 2; ++h) {
                         if (((vote >> (16 * h)) & 0xffffu) == 0u) continue;
                         const int row = 2 * warp + h + 16 * i;
-                        if constexpr (RP > 0) {
+                        if constexpr (LOG) {
+                            // append every key <= the row's threshold, column order
+                            const float tr = Lk[row];
+                            int c = Li[row];
+                            float2* lg = a.vlog + (slot * QT + row) * static_cast<size_t>(a.CV);
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) {
+                                const int col = lane + 32 * p;
+                                const float kv = sc[h * RT + col];
+                                const bool ok = col < rem && kv <= tr;
+                                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                                const int pos = c + __popc(bal & ((1u << lane) - 1u));
+                                if (ok && pos < a.CV)
+                                    lg[pos] = make_float2(kv, __int_as_float(static_cast<int>(t0 + col)));
+                                c += __popc(bal);
+                            }
+                            __syncwarp();
+                            if (lane == 0) Li[row] = c;
+                        } else if constexpr (RP > 0) {
                             float ck[4];
                             int32_t ci[4];
 #pragma unroll
@@ -288,6 +325,15 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
         }
         __syncwarp();
 
+        if constexpr (LOG) {  // the segment's log lengths (> CV: overflowed)
+            __syncwarp();
+            if (lane < 16) {
+                const int row = 2 * warp + (lane & 1) + 16 * (lane >> 1);
+                if (b * QT + row < n_eff) a.vlog_n[slot * QT + row] = Li[row];
+            }
+            __syncwarp();
+            continue;
+        }
         // emit this warp's lists: final rows when this segment is the block's
         // only one, else raw keys into the segment's slot for merge_exact
         for (int i = 0; i < 8; ++i)
@@ -443,6 +489,21 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
 
 }  // namespace
 
+template <int M>
+void launch_exact_log_m(const ExactArgs& a_in, cudaStream_t stream) {
+    ExactArgs a = a_in;
+    const size_t smem = smem_bytes(a.k, false) + 2 * QT * sizeof(float);
+    a.max_ctas = kSmCount * (smem <= 113 * 1024 ? 2 : 1);
+    auto kern = exact_knn_kernel<M, kLogKP>;
+    KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    {
+        ProfileScope ps(stream, "exact_log_kernel");
+        KNN_CUDA_CHECK(launch_kernel(kern, a.max_ctas, THREADS, smem, stream, false, a));
+    }
+    KNN_LAUNCH_CHECK();
+}
+
 size_t exact_smem_list_limit_k() {
     // lists in shared memory while 128 queries x k x 8 B + the stages fit 227 KB
     return 128;
@@ -461,6 +522,14 @@ int64_t exact_slots(int64_t n, int ntiles, int max_ctas) {
 }
 
 int exact_queries_per_cta() { return QT; }
+
+void launch_exact_log(int metric, const ExactArgs& a, cudaStream_t stream) {
+    switch (metric) {
+        case kL1: launch_exact_log_m<kL1>(a, stream); break;
+        case kLinf: launch_exact_log_m<kLinf>(a, stream); break;
+        default: launch_exact_log_m<kL2>(a, stream); break;
+    }
+}
 
 void launch_exact(int metric, const ExactArgs& a, cudaStream_t stream) {
     switch (metric) {

@@ -28,6 +28,14 @@ struct ExactArgs {
     float* mglist_key;       // merge list scratch (n x k) when k > 2048
     int64_t* mglist_idx;
     int max_ctas;            // set by launch_exact (grid of the exact kernel)
+    // threshold-log mode (large k, exact_large.cu): instead of lists, every key
+    // <= t0[q * t0_stride] is appended as {key, index bits} to the segment's
+    // log vlog[slot][128][CV] (column order), its length to vlog_n[slot][128]
+    const float* t0;
+    int t0_stride;
+    float2* vlog;
+    int* vlog_n;
+    int CV;
 };
 
 // Stream-K split of the exact path, a pure function of the query count so the
@@ -56,6 +64,8 @@ int64_t exact_slots(int64_t n, int ntiles, int max_ctas);
 // exact kernel (grid = max CTAs; the CTAs past the split's G exit) followed by
 // merge_exact when some block spans several CTAs (always when qcount is set)
 void launch_exact(int metric, const ExactArgs& a, cudaStream_t stream);
+// the threshold-log pass of the exact path (no merge; a.vlog etc. set)
+void launch_exact_log(int metric, const ExactArgs& a, cudaStream_t stream);
 size_t exact_smem_list_limit_k();
 int exact_queries_per_cta();
 

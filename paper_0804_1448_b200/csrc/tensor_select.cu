@@ -11,12 +11,15 @@
 #include "profile.cuh"
 #include "sm100.cuh"
 #include "tensor_internal.cuh"
+#include "select_common.cuh"
 #include "warp_list.cuh"
 
 namespace knnb200 {
 namespace tp {
 
 namespace {
+
+using namespace sel;
 
 // Large-k selection, one 256-thread block per query: gather the query's
 // logged {A, index} values, bitonic-sort them by A, A_(k) = k-th; certify
@@ -25,205 +28,6 @@ namespace {
 #ifndef KNN_DBG_LARGE
 #define KNN_DBG_LARGE 0
 #endif
-
-// Bitonic sort of N (power of two) (key, index) pairs in shared memory under
-// the (key, index) order, by `nthreads` threads (32: one warp, no block
-// barriers; or the whole block).  Thread t holds elements t E .. t E + E - 1 in
-// registers (E = N / nthreads): strides below E are register swaps, strides
-// below 32 E are lane shuffles, and only the strides that cross warps go
-// through shared memory (one barrier each) -- 18 barriers at N = 2048 where the
-// all-shared-memory network needs 66.
-template <int E>
-__device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) {
-    const int t = threadIdx.x;
-    const bool active = t < nthreads;
-    const int W = 32 * E;  // elements per warp
-    float rk[E];
-    int ri[E];
-    __syncthreads();  // the caller's writes of key/idx are visible
-    if (active)
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            rk[j] = key[t * E + j];
-            ri[j] = idx[t * E + j];
-        }
-    for (int size = 2; size <= N; size <<= 1) {
-        int stride = size >> 1;
-        if (stride >= W) {  // cross-warp strides (nthreads > 32 only)
-            __syncthreads();  // everyone is done reading the previous shared phase
-            if (active)
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    key[t * E + j] = rk[j];
-                    idx[t * E + j] = ri[j];
-                }
-            for (; stride >= W; stride >>= 1) {
-                __syncthreads();
-                for (int i = t; i < (N >> 1); i += blockDim.x) {
-                    const int lo = 2 * i - (i & (stride - 1));
-                    const int hi = lo + stride;
-                    const bool up = (lo & size) == 0;
-                    const float ka = key[lo], kb = key[hi];
-                    const int ia = idx[lo], ib = idx[hi];
-                    if (pair_less(kb, ib, ka, ia) == up) {
-                        key[lo] = kb;
-                        key[hi] = ka;
-                        idx[lo] = ib;
-                        idx[hi] = ia;
-                    }
-                }
-            }
-            __syncthreads();
-            if (active)
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    rk[j] = key[t * E + j];
-                    ri[j] = idx[t * E + j];
-                }
-        }
-        if (!active) continue;
-        for (; stride >= E; stride >>= 1) {  // partner in lane ^ (stride / E), same slot
-            const int lm = stride / E;
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const float pk = __shfl_xor_sync(0xffffffffu, rk[j], lm);
-                const int pi = __shfl_xor_sync(0xffffffffu, ri[j], lm);
-                const int e = t * E + j;
-                const bool keep_min = ((e & stride) == 0) == ((e & size) == 0);
-                const bool p_less = pair_less(pk, pi, rk[j], ri[j]);
-                if (p_less == keep_min) {
-                    rk[j] = pk;
-                    ri[j] = pi;
-                }
-            }
-        }
-#pragma unroll
-        for (int s = E / 2; s > 0; s >>= 1) {  // partner in this thread
-            if (s > stride) continue;
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                if (j & s) continue;
-                const bool up = ((t * E + j) & size) == 0;
-                if (pair_less(rk[j + s], ri[j + s], rk[j], ri[j]) == up) {
-                    const float tk = rk[j];
-                    const int ti = ri[j];
-                    rk[j] = rk[j + s];
-                    ri[j] = ri[j + s];
-                    rk[j + s] = tk;
-                    ri[j + s] = ti;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (active)
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            key[t * E + j] = rk[j];
-            idx[t * E + j] = ri[j];
-        }
-    __syncthreads();
-}
-
-// N (power of two, 32 <= N <= 16 * blockDim.x) pairs by the whole block:
-// one element per thread up to N = blockDim.x, then N / blockDim.x.
-__device__ void bitonic_sort_kv(float* key, int* idx, int N) {
-    const int bd = static_cast<int>(blockDim.x);
-    if (N <= bd) {
-        bitonic_sort_kv_regs<1>(key, idx, N, N);
-        return;
-    }
-    switch (N / bd) {
-        case 2: bitonic_sort_kv_regs<2>(key, idx, N, bd); break;
-        case 4: bitonic_sort_kv_regs<4>(key, idx, N, bd); break;
-        case 8: bitonic_sort_kv_regs<8>(key, idx, N, bd); break;
-        default: bitonic_sort_kv_regs<16>(key, idx, N, bd); break;
-    }
-}
-
-// k-th smallest (1-based) of x[0..n) (finite floats), block-wide radix select
-// on enc() bits, most significant digit first.  hist: 256 shared counters.
-__device__ float block_kth_smallest(const float* x, int n, int k, unsigned* hist, int* scratch) {
-    unsigned prefix = 0, mask = 0;
-    int want = k;  // rank still to find among keys matching prefix
-#pragma unroll 1
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
-        __syncthreads();
-        // warp-aggregated increments: the leading digits of nearby keys
-        // coincide, so plain atomics would serialise on one or two bins
-        for (int e0 = 0; e0 < n; e0 += blockDim.x) {
-            const int e = e0 + threadIdx.x;
-            int bin = -1;
-            if (e < n) {
-                const unsigned u = enc(x[e]);
-                if ((u & mask) == prefix) bin = static_cast<int>((u >> shift) & 255u);
-            }
-            const unsigned same = __match_any_sync(0xffffffffu, bin);
-            if (bin >= 0 && (__ffs(same) - 1) == (threadIdx.x & 31))
-                atomicAdd(hist + bin, static_cast<unsigned>(__popc(same)));
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {  // warp 0: the bin holding rank `want` (8 bins per lane)
-            const int l = threadIdx.x;
-            unsigned c[8], tot = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                c[j] = hist[8 * l + j];
-                tot += c[j];
-            }
-            unsigned incl = tot;  // inclusive prefix over lanes
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (l >= o) incl += y;
-            }
-            const unsigned excl = incl - tot;
-            if (excl < static_cast<unsigned>(want) && static_cast<unsigned>(want) <= incl) {
-                unsigned acc = excl;
-                int j = 0;
-                for (; j < 7; ++j) {
-                    if (acc + c[j] >= static_cast<unsigned>(want)) break;
-                    acc += c[j];
-                }
-                scratch[0] = 8 * l + j;
-                scratch[1] = want - static_cast<int>(acc);
-            }
-        }
-        __syncthreads();
-        const unsigned b = static_cast<unsigned>(scratch[0]);
-        want = scratch[1];
-        prefix |= b << shift;
-        mask |= 255u << shift;
-        __syncthreads();
-    }
-    return dec(prefix);
-}
-
-// Block-wide exclusive prefix sum of one int per thread (NT threads); the
-// block total in *total.  Contains barriers: every thread must call it.
-template <int NT>
-__device__ int block_exclusive_scan(int v, int* total) {
-    __shared__ int s_w[NT / 32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    __syncthreads();  // s_w of a previous call has been read
-    if (lane == 31) s_w[w] = incl;
-    __syncthreads();
-    int base = incl - v, tot = 0;
-#pragma unroll
-    for (int x = 0; x < NT / 32; ++x) {
-        base += x < w ? s_w[x] : 0;
-        tot += s_w[x];
-    }
-    *total = tot;
-    return base;
-}
 
 // NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
 // capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
