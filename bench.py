@@ -351,7 +351,10 @@ def dominant_roofline(name, per_launch_ms, launches, cfg, m_local, world, peaks,
     else:
         src = "bf16 dense" if out["bound"] == "tensor" else "hbm"
         out["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json {src})"
-    out["traffic"] = measured_traffic(name)
+    # the committed ncu capture is of config B (m = n = 38400, d = 96, k = 20):
+    # its DRAM bytes describe that shape only
+    shape_b = (cfg.get("m"), cfg.get("n"), cfg.get("d"), cfg.get("k")) == (38400, 38400, 96, 20)
+    out["traffic"] = measured_traffic(name) if shape_b and world == 1 else None
     return out
 
 
