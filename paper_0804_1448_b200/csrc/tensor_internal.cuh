@@ -296,6 +296,13 @@ struct RegList {
         key[0] = fminf(x, key[0]);
         cnt = min(cnt + 1, KR);
     }
+    // insert that leaves cnt alone for +inf ("nothing to insert" in a SIMT round)
+    __device__ __forceinline__ void insert_maybe(float x) {
+#pragma unroll
+        for (int s = KR - 1; s > 0; --s) key[s] = fmaxf(key[s - 1], fminf(x, key[s]));
+        key[0] = fminf(x, key[0]);
+        cnt = min(cnt + (x < kInf ? 1 : 0), KR);
+    }
     // key[k-1] for a runtime k.  The select chain is opaque inline PTX: written
     // as plain C++ the compiler turns it back into key[k-1], a dynamic index
     // that demotes the whole list to local memory.
