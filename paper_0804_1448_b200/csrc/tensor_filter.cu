@@ -145,9 +145,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 #define KNN_FLUSH()                                                                              \
     do {                                                                                         \
-        float* pa_ = a.part_A + static_cast<int64_t>(part) * a.Kq * TILE;                        \
+        /* row-major per query ([part][row][Kq]): the re-rank reads a list */                 \
+        /* with one coalesced load instead of Kq lines */                                       \
+        float* pa_ = a.part_A + (static_cast<int64_t>(part) * TILE + row) * a.Kq;                \
         _Pragma("unroll") for (int e_ = 0; e_ < KR; ++e_)                                        \
-            if (e_ < L.cnt) pa_[e_ * TILE + row] = L.key[e_];                                    \
+            if (e_ < L.cnt) pa_[e_] = L.key[e_];                                                 \
         a.part_cnt[part * TILE + row] = L.cnt;                                                   \
         a.log_n[part * TILE + row] = ln > a.CG - 16 ? a.CG + 1 : ln; /* (nearly) full: overflow */ \
     } while (0)

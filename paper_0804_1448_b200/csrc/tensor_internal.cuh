@@ -111,7 +111,7 @@ struct FilterArgs {
     const float* rnorm;    // no-fold norms
     const unsigned* gmax;
     unsigned* tglob;       // [n_pad] shared running threshold (ordered-uint, atomicMin)
-    float* part_A;         // [parts][Kq][128] final bound list (keys) of each part
+    float* part_A;         // [parts][128][Kq] final bound list (keys) of each part
     int* part_cnt;         // [parts][128] entries in part_A
     int* log_n;            // [parts][128] groups logged (may exceed CG: overflow)
     float4* log_v;         // [parts][128][CG][2] the 8 A values of each logged group
@@ -228,6 +228,12 @@ __device__ __forceinline__ void ldg8_hint(const float* p, float (&v)[8], uint64_
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
                    "=f"(v[6]), "=f"(v[7])
                  : "l"(p), "l"(pol));
+}
+
+__device__ __forceinline__ int2 ldg2_hint(const int* p, uint64_t pol) {
+    int2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
 }
 
 __device__ __forceinline__ int ldg_hint(const int* p, uint64_t pol) {
@@ -486,7 +492,7 @@ struct RerankArgs {
 
 __host__ __device__ constexpr size_t rr_warp_bytes(int span, int k) {
     return ((static_cast<size_t>(span) * 4 + RR_CAND * 8 + static_cast<size_t>(k) * 4 + 15) / 16) * 16 +
-           static_cast<size_t>(k) * 8;
+           static_cast<size_t>(k) * 8 + RR_CAND * 4;
 }
 
 struct Layout {

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     float* fk = reinterpret_cast<float*>(ci + RR_CAND);        // [k] result keys
     int64_t* fi = reinterpret_cast<int64_t*>(
         wb + ((static_cast<size_t>(span) * 4 + RR_CAND * 8 + static_cast<size_t>(k) * 4 + 15) / 16) * 16);
+    int* gcol = reinterpret_cast<int*>(fi + k);                // [RR_CAND] first column of in-tau groups
 
     const int qt = static_cast<int>(q / TILE);
     const int row = static_cast<int>(q % TILE);
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     float pa[2];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
-        pa[p] = (p < parts && lane < Kq) ? a.f.part_A[((p0 + p) * Kq + lane) * TILE + row] : kInf;
+        pa[p] = (p < parts && lane < Kq) ? a.f.part_A[((p0 + p) * TILE + row) * Kq + lane] : kInf;
     if (lane >= nslots) cnt = nlog = 0;
     const Consts qc = load_consts(a.f, q);
     // 0. all bound lists, compacted: list p's entries go to [excl_p, excl_p + cnt_p)
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         const int cp = __shfl_sync(0xffffffffu, cnt, p);
         const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
         if (lane < cp)
-            sv[ep + lane] = p < 2 ? pa[p] : a.f.part_A[((p0 + p) * Kq + lane) * TILE + row];
+            sv[ep + lane] = p < 2 ? pa[p] : a.f.part_A[((p0 + p) * TILE + row) * Kq + lane];
     }
     __syncwarp();
 
@@ -161,12 +162,13 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         __syncwarp();
         for (int t0 = 0; t0 < NT; t0 += 256) {
             float hv[8];
-            int hs[8];
+            int hs[8], hc[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int t = t0 + e * 32 + lane;
                 hv[e] = kInf;
                 hs[e] = 0;
+                hc[e] = 0;
                 if (t < NT) {
                     int p = 0, ex = 0;
                     for (int pp = 0; pp + 1 < nslots; ++pp) {
@@ -179,7 +181,11 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
                     // part-relative handle (part << 16 | slot, CG <= 4096): the global
                     // slot needs 64 bits once parts * 128 * CG >= 2^31
                     hs[e] = (p << 16) | (t - ex);
-                    hv[e] = __int_as_float(ldg_hint(head_of(log_slot(hs[e])), pol));
+                    // the whole head {minimum, first column}: the column of an
+                    // in-tau group is then at hand for the value step
+                    const int2 h2 = ldg2_hint(head_of(log_slot(hs[e])), pol);
+                    hv[e] = __int_as_float(h2.x);
+                    hc[e] = h2.y;
                 }
             }
 #pragma unroll
@@ -187,7 +193,10 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
                 const bool in = hv[e] <= tau;
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
                 const int pos = ng + __popc(bal & ((1u << lane) - 1u));
-                if (in && pos < RR_CAND) gl[pos] = hs[e];
+                if (in && pos < RR_CAND) {
+                    gl[pos] = hs[e];
+                    gcol[pos] = hc[e];
+                }
                 ng += __popc(bal);
             }
         }
@@ -202,7 +211,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
             if (j < ng) {
                 const int64_t slot = log_slot(gl[j]);
                 ldg8_hint(reinterpret_cast<const float*>(a.f.log_v + 2 * slot), w, pol);
-                c0 = ldg_hint(head_of(slot) + 1, pol);
+                c0 = gcol[j];
             }
             __syncwarp();
 #pragma unroll
