@@ -339,9 +339,12 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     sz.take<int64_t>(static_cast<size_t>(n) * k);
     sz.take<unsigned long long>(2);
     sz.take<int>(static_cast<size_t>(n) + 1);
-    const size_t fb_part = k <= 32 ? fallback_part_elems(n, m, k) : 0;
+    const size_t fb_part = fallback_part_elems(n, m, k);
+    const size_t fb_glist = fallback_glist_elems(k);
     sz.take<float>(fb_part);
     sz.take<int64_t>(fb_part);
+    sz.take<float>(fb_glist);
+    sz.take<int32_t>(fb_glist);
     ctx.s->io.reserve(sz.used + 256);
     ctx.s->refs.reserve(tensor_refs_bytes(m, d));
     Carver cv{static_cast<char*>(ctx.s->io.base())};
@@ -353,6 +356,8 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
     float* fb_pk = cv.take<float>(fb_part);
     int64_t* fb_pi = cv.take<int64_t>(fb_part);
+    float* fb_gk = cv.take<float>(fb_glist);
+    int32_t* fb_gi = cv.take<int32_t>(fb_glist);
     KNN_CUDA_CHECK(cudaMemsetAsync(dbad, 0xff, 2 * sizeof(unsigned long long), s));
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), s));
     // every H2D goes through the copy stream in order (R, then the query
@@ -404,7 +409,7 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     }
     // uncertified queries of all chunks, resolved once over the whole query
     // set (small k on the device: exact kernel over the recorded list)
-    tensor_resolve_fallbacks(ctx, s, refs, dQ, n, k, raw_keys, 0, dO, dI, fb, fb_pk, fb_pi);
+    tensor_resolve_fallbacks(ctx, s, refs, dQ, n, k, raw_keys, 0, dO, dI, fb, fb_pk, fb_pi, fb_gk, fb_gi);
     unsigned long long bad[2];
     int fails = 0;
     KNN_CUDA_CHECK(cudaMemcpyAsync(bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost, s));

@@ -175,11 +175,4 @@ void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int
     run_exact(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);
 }
 
-// exposed for the tensor path's fallback on uncertified queries
-void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
-                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
-                      float* d_out, int64_t* d_idx) {
-    run_exact(ctx, stream, dQ, n, dR, m, d, k, kL2, raw_keys, index_base, d_out, d_idx);
-}
-
 }  // namespace knnb200

@@ -445,11 +445,15 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
     const size_t smem = smem_bytes(a.k, smem_lists);
     a.max_ctas = exact_max_ctas(a.k, smem_lists);
     const int kp = (a.k + 31) / 32;
-    void (*kern)(ExactArgs) = !smem_lists ? (a.k <= 256 ? exact_knn_kernel<M, -8> : exact_knn_kernel<M, 0>)
-                              : kp == 1   ? (a.qlist ? exact_knn_kernel<M, 1, true> : exact_knn_kernel<M, 1>)
-                              : kp == 2   ? exact_knn_kernel<M, 2>
-                                          : exact_knn_kernel<M, 4>;
-    if (a.qlist && !(smem_lists && kp == 1)) throw CudaError("exact kernel: query lists need k <= 32");
+    // INDIRECT (query list, device-side count): the certification fallback of
+    // the tensor path, small and large k
+    const bool ind = a.qlist != nullptr;
+    void (*kern)(ExactArgs) =
+        !smem_lists ? (a.k <= 256 ? (ind ? exact_knn_kernel<M, -8, true> : exact_knn_kernel<M, -8>)
+                                  : (ind ? exact_knn_kernel<M, 0, true> : exact_knn_kernel<M, 0>))
+        : kp == 1   ? (ind ? exact_knn_kernel<M, 1, true> : exact_knn_kernel<M, 1>)
+        : kp == 2   ? (ind ? exact_knn_kernel<M, 2, true> : exact_knn_kernel<M, 2>)
+                    : (ind ? exact_knn_kernel<M, 4, true> : exact_knn_kernel<M, 4>);
     KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {

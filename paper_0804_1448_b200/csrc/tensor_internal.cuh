@@ -563,10 +563,5 @@ void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const Fil
                          int G, size_t smem, cudaStream_t stream);
 void launch_select_large(const LargeArgs& la, cudaStream_t stream);
 void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream);
-void launch_gather_rows(const float* X, int d, const int* list, int count, float* out,
-                        cudaStream_t stream);
-void launch_scatter_rows(const float* src_d, const int64_t* src_i, const int* list, int count,
-                         int k, float* out, int64_t* out_idx, cudaStream_t stream);
-
 }  // namespace tp
 }  // namespace knnb200

@@ -22,10 +22,9 @@
 //               union of the part lists, certificate, exact FP32 keys of the
 //               logged candidates, exact top-k.  Large k (tensor_select.cu):
 //               block per query, radix select, exact keys, bitonic sort.
-//  4. fallback  uncertified queries are recomputed by the exact SIMT kernel --
-//               on the device for small k (no host round trip), host-driven
-//               with one re-seeded retry for large k.  Results are bitwise
-//               identical to the exact path.
+//  4. fallback  uncertified queries are recomputed by the exact SIMT kernel
+//               on the device (query list and count in HBM, no host round
+//               trip).  Results are bitwise identical to the exact path.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -113,7 +112,7 @@ void run_tensor_path(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
 
 void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
                    const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
-                   float* d_out, int64_t* d_idx, const FallbackSink* sink, int margin, bool retry) {
+                   float* d_out, int64_t* d_idx, const FallbackSink* sink, int margin) {
     const float* dR = refs.dR;
     const int64_t m = refs.m;
     const int d = refs.d;
@@ -125,7 +124,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     const int64_t m_pad = static_cast<int64_t>(rtiles) * TILE;
     const int64_t U = static_cast<int64_t>(pairs) * rtiles;
     const bool large = k > MAX_KQ;
-    if (large && !retry)
+    if (large)
         if (const char* e = std::getenv("KNN_B200_LARGE_MARGIN")) margin = std::max(1, std::atoi(e));  // dev
     // at most ~29 CTAs share a query-tile pair, so a query has <= 32 partial lists
     const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
@@ -166,9 +165,15 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     sz.take<int>(static_cast<size_t>(pairs));
     // small k: the certification fallback runs on the device (exact kernel over
     // the failed queries, count read on the device): its partial-list slots
-    const size_t fb_part = large ? 0 : fallback_part_elems(n, m, k);
+    // the certification fallback runs on the device (exact kernel over the
+    // failed queries, count read on the device): its partial-list slots, and
+    // for k > 128 its global list scratch
+    const size_t fb_part = fallback_part_elems(n, m, k);
+    const size_t fb_glist = fallback_glist_elems(k);
     sz.take<float>(fb_part);
     sz.take<int64_t>(fb_part);
+    sz.take<float>(fb_glist);
+    sz.take<int32_t>(fb_glist);
     ctx.s->arena.reserve(sz.used + 256);
     Carver cv{static_cast<char*>(ctx.s->arena.base())};
     __half* Qh = cv.take<__half>(static_cast<size_t>(n_pad) * L.Kp);
@@ -187,6 +192,8 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     int* pair_slots = cv.take<int>(static_cast<size_t>(pairs));
     float* fb_pk = cv.take<float>(fb_part);
     int64_t* fb_pi = cv.take<int64_t>(fb_part);
+    float* fb_gk = cv.take<float>(fb_glist);
+    int32_t* fb_gi = cv.take<int32_t>(fb_glist);
     const unsigned* gmax = refs.gmax;
 
     // 1. per-search state and the query-side prep
@@ -265,7 +272,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         fa.seed_rank = 32;
         fa.W = static_cast<int>(std::min<int64_t>(
             rtiles, std::max<int64_t>(2, (m + 4LL * margin * k - 1) / (4LL * margin * k))));
-        fa.seed_off = retry ? 1 : 0;
+        fa.seed_off = 0;
         fa.t0 = t0;
         fa.vlog = vlog;
         fa.CV = CV;
@@ -341,77 +348,53 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     //    the caller collects them across several searches.
     if (sink) return;
     tensor_resolve_fallbacks(ctx, stream, refs, dQ, n, k, raw_keys, index_base, d_out, d_idx, fb,
-                             fb_pk, fb_pi, margin, retry);
+                             fb_pk, fb_pi, fb_gk, fb_gi);
 }
 
+static bool fallback_smem_lists(int k) { return static_cast<size_t>(k) <= exact_smem_list_limit_k(); }
+
 size_t fallback_part_elems(int64_t n, int64_t m, int k) {
-    return static_cast<size_t>(exact_slots(n, exact_ntiles(m), exact_max_ctas(k, true))) *
+    return static_cast<size_t>(exact_slots(n, exact_ntiles(m), exact_max_ctas(k, fallback_smem_lists(k)))) *
            exact_queries_per_cta() * k;
+}
+
+size_t fallback_glist_elems(int k) {
+    return fallback_smem_lists(k) ? 0
+                                  : static_cast<size_t>(exact_max_ctas(k, false)) * exact_queries_per_cta() * k;
 }
 
 void tensor_resolve_fallbacks(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
                               const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
                               float* d_out, int64_t* d_idx, int* fb, float* fb_pk, int64_t* fb_pi,
-                              int margin, bool retry) {
-    const float* dR = refs.dR;
-    const int64_t m = refs.m;
-    const int d = refs.d;
-    // Small k: entirely on the device -- the exact kernel reads the failed
-    // query list and its count from HBM (fixed grid), no host round trip, so
-    // the search stays asynchronous and graph-capturable.
-    if (k <= MAX_KQ) {
-        ExactArgs ea{};
-        ea.Q = dQ;
-        ea.R = dR;
-        ea.n = n;
-        ea.m = m;
-        ea.d = d;
-        ea.k = k;
-        ea.ntiles = exact_ntiles(m);
-        ea.qlist = fb + 1;
-        ea.qcount = fb;
-        ea.index_base = index_base;
-        ea.raw_keys = raw_keys;
-        ea.out_key = d_out;
-        ea.out_idx = d_idx;
-        ea.part_key = fb_pk;
-        ea.part_idx = fb_pi;
-        launch_exact(kL2, ea, stream);
-        if (ctx.s->fb_dev)
-            KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        ctx.s->fb_on_device = true;
-        return;
+                              float* fb_gk, int32_t* fb_gi) {
+    // On the device for every k: the exact kernel reads the failed query list
+    // and its count from HBM (fixed grid), merge_exact finishes the blocks it
+    // spread over several CTAs -- no host round trip, so the search stays
+    // asynchronous and graph-capturable.
+    ExactArgs ea{};
+    ea.Q = dQ;
+    ea.R = refs.dR;
+    ea.n = n;
+    ea.m = refs.m;
+    ea.d = refs.d;
+    ea.k = k;
+    ea.ntiles = exact_ntiles(refs.m);
+    ea.qlist = fb + 1;
+    ea.qcount = fb;
+    ea.index_base = index_base;
+    ea.raw_keys = raw_keys;
+    ea.out_key = d_out;
+    ea.out_idx = d_idx;
+    ea.part_key = fb_pk;
+    ea.part_idx = fb_pi;
+    if (fallback_glist_elems(k) > 0) {  // k > 128: lists in global memory
+        ea.glist_key = fb_gk;
+        ea.glist_idx = fb_gi;
     }
-    ctx.s->fb_on_device = false;
-    int fails = 0;
-    KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
-    if (fails > 0) {
-        // the fallback allocates its own scratch: keep the gathered queries in a
-        // dedicated buffer so the exact path's arena use cannot clobber them
-        // (the list too: fb may live in the arena the nested search reuses)
-        float* gq = nullptr;
-        float* od = nullptr;
-        int64_t* oi = nullptr;
-        int* dl = nullptr;
-        KNN_CUDA_CHECK(cudaMallocAsync(&gq, sizeof(float) * fails * d, stream));
-        KNN_CUDA_CHECK(cudaMallocAsync(&od, sizeof(float) * fails * k, stream));
-        KNN_CUDA_CHECK(cudaMallocAsync(&oi, sizeof(int64_t) * fails * k, stream));
-        KNN_CUDA_CHECK(cudaMallocAsync(&dl, sizeof(int) * fails, stream));
-        KNN_CUDA_CHECK(cudaMemcpyAsync(dl, fb + 1, sizeof(int) * fails, cudaMemcpyDeviceToDevice, stream));
-        launch_gather_rows(dQ, d, dl, fails, gq, stream);
-        if (!retry)  // a tail estimate of T0: once more from fresh seed tiles
-            tensor_search(ctx, stream, refs, gq, fails, k, raw_keys, index_base, od, oi, nullptr,
-                          margin, true);
-        else
-            run_exact_subset(ctx, stream, gq, fails, dR, m, d, k, raw_keys, index_base, od, oi);
-        launch_scatter_rows(od, oi, dl, fails, k, d_out, d_idx, stream);
-        KNN_CUDA_CHECK(cudaFreeAsync(dl, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(gq, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(od, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(oi, stream));
-    }
-    ctx.s->last_fallbacks = fails;
+    launch_exact(kL2, ea, stream);
+    if (ctx.s->fb_dev)
+        KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+    ctx.s->fb_on_device = true;
 }
 
 }  // namespace knnb200

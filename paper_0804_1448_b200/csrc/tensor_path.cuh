@@ -41,27 +41,21 @@ struct FallbackSink {
     int offset;
 };
 
-// margin: large-k threshold target, T0 ~ the (margin*k)-th smallest A; the
-// large-k certification fallback retries once (retry = true) from fresh seed
-// tiles before the exact path.
+// margin: large-k threshold target, T0 ~ the (margin*k)-th smallest A.
 void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
                    const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
                    float* d_out, int64_t* d_idx, const FallbackSink* sink = nullptr,
-                   int margin = 3, bool retry = false);
+                   int margin = 3);
 
 // Resolve the certification fallbacks recorded in fb ({count, query list}) of
-// a search over dQ (n rows): small k on the device (exact kernel over the
-// list; fb_pk / fb_pi: fallback_part_elems(n, m, k) partial-list slots), large
-// k host-driven (one re-seeded retry, then the exact path).
+// a search over dQ (n rows) on the device: the exact kernel over the list
+// (fb_pk / fb_pi: fallback_part_elems(n, m, k) partial-list slots; fb_gk /
+// fb_gi: fallback_glist_elems(k) list scratch, k > 128).
 size_t fallback_part_elems(int64_t n, int64_t m, int k);
+size_t fallback_glist_elems(int k);
 void tensor_resolve_fallbacks(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& refs,
                               const float* dQ, int64_t n, int k, int raw_keys, int64_t index_base,
                               float* d_out, int64_t* d_idx, int* fb, float* fb_pk, int64_t* fb_pi,
-                              int margin = 3, bool retry = false);
-
-// exact path on a subset of queries (certification fallback), defined in engine.cu
-void run_exact_subset(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
-                      const float* dR, int64_t m, int d, int k, int raw_keys, int64_t index_base,
-                      float* d_out, int64_t* d_idx);
+                              float* fb_gk, int32_t* fb_gi);
 
 }  // namespace knnb200

@@ -281,25 +281,6 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
     }
 }
 
-// gather / scatter for the certification fallback
-__global__ void gather_rows_kernel(const float* X, int d, const int* list, int count, float* out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t total = static_cast<int64_t>(count) * d;
-    if (i >= total) return;
-    const int64_t r = i / d;
-    out[i] = X[static_cast<int64_t>(list[r]) * d + i % d];
-}
-
-__global__ void scatter_rows_kernel(const float* src_d, const int64_t* src_i, const int* list,
-                                    int count, int k, float* out, int64_t* out_idx) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= static_cast<int64_t>(count) * k) return;
-    const int64_t r = i / k;
-    const int64_t dst = static_cast<int64_t>(list[r]) * k + i % k;
-    out[dst] = src_d[i];
-    out_idx[dst] = src_i[i];
-}
-
 }  // namespace
 
 void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream) {
@@ -308,28 +289,6 @@ void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream) {
         KNN_CUDA_CHECK(launch_kernel(rerank_kernel,
                                      static_cast<unsigned>((ra.n + RR_WARPS - 1) / RR_WARPS),
                                      RR_WARPS * 32, smem, stream, pdl_enabled(2), ra));
-    }
-    KNN_LAUNCH_CHECK();
-}
-
-void launch_gather_rows(const float* X, int d, const int* list, int count, float* out,
-                        cudaStream_t stream) {
-    const int64_t tot = static_cast<int64_t>(count) * d;
-    {
-        ProfileScope ps(stream, "fallback_gather");
-        gather_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(X, d, list,
-                                                                                       count, out);
-    }
-    KNN_LAUNCH_CHECK();
-}
-
-void launch_scatter_rows(const float* src_d, const int64_t* src_i, const int* list, int count,
-                         int k, float* out, int64_t* out_idx, cudaStream_t stream) {
-    const int64_t tot = static_cast<int64_t>(count) * k;
-    {
-        ProfileScope ps(stream, "fallback_scatter");
-        scatter_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
-            src_d, src_i, list, count, k, out, out_idx);
     }
     KNN_LAUNCH_CHECK();
 }

@@ -394,11 +394,29 @@ def test_tensor_path_extreme_magnitudes(knn, oracle, case):
 
 
 @pytest.mark.gpu
-def test_index_search_captures_into_a_cuda_graph(knn, oracle):
-    """An index search on a caller stream (k <= 32: no host round trip) can be
-    captured into a CUDA graph; replays give the eager result bitwise."""
+@pytest.mark.parametrize("k", [64, 300])
+def test_large_k_fallback_on_device(knn, oracle, k):
+    """Large k (fixed-threshold filter + block selection): one point repeated
+    fills every log, the certificate fails for every query and the exact
+    kernel recomputes them from the device-side query list (no host round
+    trip) -- the table is the exact path's, bitwise."""
+    Qd = oracle.uniform_f32(50, 16, 734)
+    Rs = np.repeat(oracle.uniform_f32(1, 16, 735), 40000, axis=0)
+    ts = knn.bf_knn(Qd, Rs, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() > 0
+    tse = knn.bf_knn(Qd, Rs, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (ts.index == tse.index).all() and (ts.distance == tse.distance).all()
+    assert (ts.index == np.arange(k)[None, :]).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [16, 100])
+def test_index_search_captures_into_a_cuda_graph(knn, oracle, k):
+    """An index search on a caller stream (no host round trip for any k,
+    certification fallbacks included) can be captured into a CUDA graph;
+    replays give the eager result bitwise."""
     import torch
-    n, m, d, k = 2000, 20000, 40, 16
+    n, m, d = 2000, 20000, 40
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         Q = torch.from_numpy(oracle.uniform_f32(n, d, 91)).cuda()
