@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // (compact {A, index} records, predicated stores).  T0 is only an estimate;
 // the selection kernel certifies it (at least k logged values and
 // thresh(A_(k)) <= T0, no log overflow) and sends the rest to the exact path.
-template <int DUMMY>
+template <bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_fixed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
                         FilterArgs a) {
@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                static_cast<uint32_t>(2 * grp * TILE);
         RegList<32> S;  // seed: the 32 smallest seed group minima
         S.reset();
-        float T0 = kInf;
+        float T0 = kInf;   // the segment's fixed threshold (after its seed units)
+        float tlog = kInf; // T0, or -inf once the log is (nearly) full
         Consts qc{};
         int64_t q = 0, part = 0;
         float2* vlp = nullptr;
@@ -374,14 +375,42 @@ __global__ void __launch_bounds__(THREADS, 1)
         int64_t t = 0;
         UnitSeq sq;
         sq.init(u_begin, u_end, a.rtiles, a.W, a.seed_off);
-        // no-fold layouts: reference norms staged per unit (see filter_kernel)
         float* const rnw = RN + (warp - 4) * TILE;
         float4 rn_nx = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!a.fold && sq.more())
+        if (!FOLD && sq.more())
             rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + sq.tile() * TILE) + lane);
-        auto finish = [&]() {
-            a.log_n[part * TILE + row] = ln;
-        };
+        auto finish = [&]() { a.log_n[part * TILE + row] = ln; };
+
+        // Log every value of a 32-column chunk at or under tlog: if some lane of
+        // the warp has a value there, 3-instruction predicated appends of all 32
+        // ({A, index} records, the cursor advanced in the same PTX block).
+#define KNN_LOG32(rr, colb)                                                                      \
+    do {                                                                                         \
+        float v_[32];                                                                            \
+        _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
+        if (!FOLD) add_rnorm_smem(v_, rnw + ((colb) - col_base));                                \
+        float m_[11];                                                                            \
+        _Pragma("unroll") for (int i_ = 0; i_ < 10; ++i_)                                        \
+            m_[i_] = min3(v_[3 * i_], v_[3 * i_ + 1], v_[3 * i_ + 2]);                           \
+        m_[10] = fminf(v_[30], v_[31]);                                                          \
+        const float cm_ = min3(min3(m_[0], m_[1], m_[2]), min3(m_[3], m_[4], m_[5]),             \
+                               min3(min3(m_[6], m_[7], m_[8]), m_[9], m_[10]));                  \
+        if (__any_sync(0xffffffffu, cm_ <= tlog)) {                                              \
+            float2* const v0_ = vlp;                                                             \
+            _Pragma("unroll") for (int e_ = 0; e_ < 32; ++e_)                                    \
+                asm volatile(                                                                    \
+                    "{\n\t.reg .pred p;\n\t"                                                     \
+                    "setp.le.f32 p, %1, %2;\n\t"                                                 \
+                    "@p st.global.v2.b32 [%0], {%1, %3};\n\t"                                    \
+                    "@p add.s64 %0, %0, 8;\n\t}"                                                 \
+                    : "+l"(vlp)                                                                  \
+                    : "f"(v_[e_]), "f"(tlog), "r"((colb) + e_)                                   \
+                    : "memory");                                                                 \
+            ln += static_cast<int>(vlp - v0_);                                                   \
+        }                                                                                        \
+    } while (0)
+
+        uint32_t ra[32], rb[32];
         for (; sq.more(); sq.next(), ++t) {
             if (sq.p != cur_p) {
                 if (cur_p >= 0) finish();
@@ -399,7 +428,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const bool seed = sq.seed();
             if (!seed && was_seed) {  // seed complete: fix the segment's threshold
                 T0 = thresh(S.kth(a.seed_rank), qc);
-                if (lane < 32) a.t0[q] = T0;  // identical from every CTA of the pair
+                a.t0[q] = T0;  // identical from every CTA of the pair
             }
             was_seed = seed;
             const int b = static_cast<int>(t & 1);
@@ -407,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             sm100::tc_fence_after();
             const uint32_t taddr = tlane + static_cast<uint32_t>(b * TILE);
             const int col_base = sq.tile() * TILE;
-            if (!a.fold) {
+            if (!FOLD) {
                 __syncwarp();
                 reinterpret_cast<float4*>(rnw)[lane] = rn_nx;
                 __syncwarp();
@@ -416,63 +445,49 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (nx.more())
                     rn_nx = __ldg(reinterpret_cast<const float4*>(a.rnorm + nx.tile() * TILE) + lane);
             }
+            auto release = [&]() {
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
+            };
+            if (seed) {  // seed unit: every group minimum into the 32-entry list
 #pragma unroll 1
-            for (int h = 0; h < 4; ++h) {  // 32-column chunks (one TMEM load each)
-                uint32_t r0[32];
-                sm100::tmem_ld_32x32b_x32(taddr + h * 32, r0);
-                sm100::tmem_ld_wait();
-                if (h == 3) {
-                    sm100::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) sm100::mbar_arrive(tempty + 2 * grp + b);
-                }
-                float v[32];
+                for (int h = 0; h < 4; ++h) {
+                    sm100::tmem_ld_32x32b_x32(taddr + h * 32, ra);
+                    sm100::tmem_ld_wait();
+                    if (h == 3) release();
+                    float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
-                const int cb = col_base + h * 32;
-                if (!a.fold) add_rnorm_smem(v, rnw + h * 32);
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
+                    if (!FOLD) add_rnorm_smem(v, rnw + h * 32);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const float* w = v + 8 * g;
-                    const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
-                    if (seed) {
-                        S.insert(gm);
-                    } else if (__any_sync(0xffffffffu, gm <= T0)) {
-                        const int col = cb + 8 * g;
-                        if (ln + 8 <= a.CV) {  // room for the whole group: 3 instructions per value
-                            float2* const v0 = vlp;
-#pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                asm volatile(
-                                    "{\n\t.reg .pred p;\n\t"
-                                    "setp.le.f32 p, %1, %2;\n\t"
-                                    "@p st.global.v2.b32 [%0], {%1, %3};\n\t"
-                                    "@p add.s64 %0, %0, 8;\n\t}"
-                                    : "+l"(vlp)
-                                    : "f"(w[e]), "f"(T0), "r"(col + e)
-                                    : "memory");
-                            ln += static_cast<int>(vlp - v0);
-                            continue;
-                        }
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const int room = ln < a.CV ? 1 : 0;
-                            asm volatile(
-                                "{\n\t.reg .pred p, q;\n\t"
-                                "setp.le.f32 p, %0, %1;\n\t"
-                                "setp.ne.and.s32 q, %2, 0, p;\n\t"
-                                "@q st.global.v2.b32 [%3], {%0, %4};\n\t}" ::"f"(w[e]),
-                                "f"(T0), "r"(room), "l"(vlp), "r"(col + e)
-                                : "memory");
-                            const int hit = w[e] <= T0 ? 1 : 0;
-                            vlp += hit;
-                            ln += hit;
-                        }
+                    for (int g = 0; g < 4; ++g) {
+                        const float* w = v + 8 * g;
+                        const float gm = fminf(min3(min3(w[0], w[1], w[2]), min3(w[3], w[4], w[5]), w[6]), w[7]);
+                        // a minimum at or above the list's last entry changes nothing
+                        if (__any_sync(0xffffffffu, gm < S.key[31])) S.insert(gm);
                     }
                 }
+                continue;
             }
+            // a unit logs <= 128 values: stop logging (the query then fails the
+            // certificate and is recomputed exactly) once fewer slots are left
+            tlog = ln > a.CV - 128 ? -kInf : T0;
+            sm100::tmem_ld_32x32b_x32(taddr, ra);
+            sm100::tmem_ld_32x32b_x32(taddr + 32, rb);
+            sm100::tmem_ld_wait();
+            KNN_LOG32(ra, col_base);
+            sm100::tmem_ld_32x32b_x32(taddr + 64, ra);
+            KNN_LOG32(rb, col_base + 32);
+            sm100::tmem_ld_wait();
+            sm100::tmem_ld_32x32b_x32(taddr + 96, rb);
+            KNN_LOG32(ra, col_base + 64);
+            sm100::tmem_ld_wait();
+            release();
+            KNN_LOG32(rb, col_base + 96);
         }
         if (cur_p >= 0) finish();
+#undef KNN_LOG32
     }
 
     sm100::pdl_trigger();
@@ -511,12 +526,12 @@ void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const F
 
 void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
                          int G, size_t smem, cudaStream_t stream) {
-    KNN_CUDA_CHECK(cudaFuncSetAttribute(filter_fixed_kernel<0>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = fa.fold ? filter_fixed_kernel<true> : filter_fixed_kernel<false>;
+    KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {
         ProfileScope ps(stream, "tc_filter_fixed_kernel");
-        KNN_CUDA_CHECK(launch_kernel(filter_fixed_kernel<0>, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
+        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
     }
     KNN_LAUNCH_CHECK();
 }
