@@ -154,7 +154,6 @@ static void run_exact(DeviceContext& ctx, cudaStream_t stream, const float* dQ, 
     }();
     if (large_ok && exact_large_applies(m, k)) {
         run_exact_large(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);
-        ctx.s->fb_on_device = false;
         return;
     }
     run_exact_lists(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx);

@@ -95,9 +95,12 @@ void run_exact_lists(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
                      int64_t index_base, float* d_out, int64_t* d_idx);
 bool exact_large_applies(int64_t m, int k);
+// (qlist, qcount): device-side query list (positions -> rows of dQ and of the
+// outputs), e.g. the tensor path's certification fallback; n = list capacity
 void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
-                     int64_t index_base, float* d_out, int64_t* d_idx);
+                     int64_t index_base, float* d_out, int64_t* d_idx, const int* qlist = nullptr,
+                     const int* qcount = nullptr);
 
 void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                    const float* dR, int64_t m, int d, int k, int metric, int path,

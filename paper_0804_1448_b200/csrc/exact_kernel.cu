@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
             if (lane < 16) {
                 const int row = 2 * warp + (lane & 1) + 16 * (lane >> 1);
                 const int64_t q = b * QT + row;
-                Lk[row] = q < n_eff ? a.t0[q * a.t0_stride] : -kInf;
+                // thresholds are indexed by the query's row in Q (its list row)
+                const int64_t orow = q < n_eff ? (INDIRECT ? static_cast<int64_t>(a.qlist[q]) : q) : 0;
+                Lk[row] = q < n_eff ? a.t0[orow * a.t0_stride] : -kInf;
                 Li[row] = 0;
             }
         } else {
@@ -497,8 +499,8 @@ template <int M>
 void launch_exact_log_m(const ExactArgs& a_in, cudaStream_t stream) {
     ExactArgs a = a_in;
     const size_t smem = smem_bytes(a.k, false) + 2 * QT * sizeof(float);
-    a.max_ctas = kSmCount * (smem <= 113 * 1024 ? 2 : 1);
-    auto kern = exact_knn_kernel<M, kLogKP>;
+    a.max_ctas = exact_log_max_ctas();
+    auto kern = a.qlist ? exact_knn_kernel<M, kLogKP, true> : exact_knn_kernel<M, kLogKP>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {
@@ -506,6 +508,11 @@ void launch_exact_log_m(const ExactArgs& a_in, cudaStream_t stream) {
         KNN_CUDA_CHECK(launch_kernel(kern, a.max_ctas, THREADS, smem, stream, false, a));
     }
     KNN_LAUNCH_CHECK();
+}
+
+int exact_log_max_ctas() {
+    const size_t smem = smem_bytes(1, false) + 2 * QT * sizeof(float);
+    return kSmCount * (smem <= 113 * 1024 ? 2 : 1);
 }
 
 size_t exact_smem_list_limit_k() {

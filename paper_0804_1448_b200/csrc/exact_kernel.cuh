@@ -66,6 +66,7 @@ int64_t exact_slots(int64_t n, int ntiles, int max_ctas);
 void launch_exact(int metric, const ExactArgs& a, cudaStream_t stream);
 // the threshold-log pass of the exact path (no merge; a.vlog etc. set)
 void launch_exact_log(int metric, const ExactArgs& a, cudaStream_t stream);
+int exact_log_max_ctas();  // grid of the threshold-log pass
 size_t exact_smem_list_limit_k();
 int exact_queries_per_cta();
 

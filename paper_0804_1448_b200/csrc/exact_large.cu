@@ -17,7 +17,11 @@
 //               A_(k) <= T0 (every key <= A_(k) is then in a log); keep the keys
 //               below A_(k) and the lowest-index ties at A_(k) (the logs are in
 //               ascending index order), sort them by (key, index), finalize.
-//   4. fallback uncertified queries (a tail estimate of T0) run the list path.
+//   4. fallback uncertified queries (a tail estimate of T0) run the list path
+//               over a device-side row list.
+// All of it is stream-ordered device work (no host round trip), and the same
+// sequence serves a device-side query list (the tensor path's large-k
+// certification fallback).
 // Results are bitwise the list path's: same keys, same (key, index) order.
 #include <algorithm>
 #include <cstdio>
@@ -48,6 +52,8 @@ __global__ void gather_strided_kernel(const float* X, int d, int64_t stride, int
 }
 
 struct SelArgs {
+    const int* qlist;   // nullable: position i of the search is Q row / output row qlist[i]
+    const int* qcount;  // nullable: device-side count of positions (<= n)
     const float2* vlog;
     const int* vlog_n;
     int CV, NC, k;
@@ -72,11 +78,15 @@ __global__ void __launch_bounds__(NT) select_exact_kernel(SelArgs a) {
     __shared__ int s_tot;
     __shared__ int s_sel[2];
     __shared__ unsigned s_hist[256];
-    const int64_t q = blockIdx.x;
+    const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
+    // block-stride over positions: a device-side count launches a fixed grid
+    for (int64_t q = blockIdx.x; q < n_eff; q += gridDim.x) {  // position (logs are by position)
+    __syncthreads();  // the previous position's shared-memory reads are done
+    const int64_t orow = a.qlist ? static_cast<int64_t>(a.qlist[q]) : q;  // Q / output row
     const int64_t b = q / 128;
     const int row = static_cast<int>(q - b * 128);
     const int k = a.k;
-    const ExactSplit sp = exact_split(a.n, a.ntiles, a.max_ctas);
+    const ExactSplit sp = exact_split(n_eff, a.ntiles, a.max_ctas);
     const int64_t first = sp.cta_of(b * a.ntiles), last = sp.cta_of((b + 1) * a.ntiles - 1);
     const int nparts = static_cast<int>(last - first + 1);
     auto part_base = [&](int p) { return (static_cast<size_t>(first + p + b) * 128 + row); };
@@ -94,7 +104,7 @@ __global__ void __launch_bounds__(NT) select_exact_kernel(SelArgs a) {
     }
     __syncthreads();
     const int total = s_tot;
-    const float T0 = a.t0[q * a.t0_stride];
+    const float T0 = a.t0[orow * a.t0_stride];
     bool ok = total >= k;
     float K = kInf;
     if (ok) {
@@ -114,9 +124,9 @@ __global__ void __launch_bounds__(NT) select_exact_kernel(SelArgs a) {
     if (!ok) {
         if (threadIdx.x == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
-            a.fb_list[slot] = static_cast<int>(q);
+            a.fb_list[slot] = static_cast<int>(orow);
         }
-        return;
+        continue;
     }
     // keep the k smallest under (key, index): keys < K, then the lowest-index
     // keys == K (the array is in ascending index order); thread t owns the
@@ -178,27 +188,10 @@ __global__ void __launch_bounds__(NT) select_exact_kernel(SelArgs a) {
         }
     }
     for (int t = threadIdx.x; t < k; t += NT) {
-        a.out[q * k + t] = sk[t];
-        a.out_idx[q * k + t] = a.index_base + si[t];
+        a.out[orow * k + t] = sk[t];
+        a.out_idx[orow * k + t] = a.index_base + si[t];
     }
-}
-
-// gather / scatter of the fallback queries
-__global__ void gather_list_kernel(const float* X, int d, const int* list, int count, float* out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= static_cast<int64_t>(count) * d) return;
-    const int64_t r = i / d;
-    out[i] = X[static_cast<int64_t>(list[r]) * d + (i - r * d)];
-}
-
-__global__ void scatter_list_kernel(const float* sd, const int64_t* si, const int* list, int count, int k,
-                                    float* out, int64_t* out_idx) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= static_cast<int64_t>(count) * k) return;
-    const int64_t r = i / k;
-    const int64_t dst = static_cast<int64_t>(list[r]) * k + (i - r * k);
-    out[dst] = sd[i];
-    out_idx[dst] = si[i];
+    }
 }
 
 }  // namespace
@@ -209,45 +202,77 @@ bool exact_large_applies(int64_t m, int k) {
 
 void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
-                     int64_t index_base, float* d_out, int64_t* d_idx) {
+                     int64_t index_base, float* d_out, int64_t* d_idx, const int* qlist,
+                     const int* qcount) {
+    // Everything below is stream-ordered device work: no host round trip, so
+    // the search is asynchronous and graph-capturable; with (qlist, qcount)
+    // it serves a device-side query list (the tensor path's certification
+    // fallback).  Outputs and thresholds are indexed by the query's row,
+    // logs by its position.
     // 1. sample: every stride-th reference, s ~ kSeedRank m / (kMargin k) rows
     const int64_t stride = std::max<int64_t>(1, (static_cast<int64_t>(kMargin) * k) / kSeedRank);
     const int64_t s = (m + stride - 1) / stride;
-    // 2. log pass scratch: per (segment slot, row) logs of CV entries
-    const int ntiles = exact_ntiles(m);
-    const int max_ctas = kSmCount * 2;
-    const int64_t slots = exact_slots(n, ntiles, max_ctas);
+    const int ntiles = exact_ntiles(m), stiles = exact_ntiles(s);
+    const int smax = exact_max_ctas(kSeedRank, true);
+    const int lmax = exact_log_max_ctas();
+    const int gmax = exact_max_ctas(k, false);
+    const int64_t s_slots = exact_slots(n, stiles, smax);
+    const int64_t l_slots = exact_slots(n, ntiles, lmax);
+    const int64_t f_slots = exact_slots(n, ntiles, gmax);
     const int CV = 2 * kMargin * k + 256;
     int NC = 1;
     while (NC < 2 * kMargin * k) NC <<= 1;
     NC = std::min(NC, 16 * 512);
     Sizer sz;
     sz.take<float>(static_cast<size_t>(s) * d);
-    sz.take<float>(static_cast<size_t>(n) * kSeedRank);
+    sz.take<float>(static_cast<size_t>(n) * kSeedRank);           // sample keys, by row
     sz.take<int64_t>(static_cast<size_t>(n) * kSeedRank);
-    sz.take<float2>(static_cast<size_t>(slots) * 128 * CV);
-    sz.take<int>(static_cast<size_t>(slots) * 128);
-    sz.take<int>(static_cast<size_t>(n) + 1);
-    const size_t own = sz.used + 256;
-    // the sample search carves the context arena, so this path's buffers come
-    // from a separate allocation (stream-ordered)
+    sz.take<float>(static_cast<size_t>(s_slots) * 128 * kSeedRank);  // sample search slots
+    sz.take<int64_t>(static_cast<size_t>(s_slots) * 128 * kSeedRank);
+    sz.take<float2>(static_cast<size_t>(l_slots) * 128 * CV);
+    sz.take<int>(static_cast<size_t>(l_slots) * 128);
+    sz.take<int>(static_cast<size_t>(n) + 1);                     // uncertified rows
+    sz.take<float>(static_cast<size_t>(f_slots) * 128 * k);        // their list-path search
+    sz.take<int64_t>(static_cast<size_t>(f_slots) * 128 * k);
+    sz.take<float>(static_cast<size_t>(gmax) * 128 * k);
+    sz.take<int32_t>(static_cast<size_t>(gmax) * 128 * k);
     char* mem = nullptr;
-    KNN_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&mem), own, stream));
+    KNN_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&mem), sz.used + 256, stream));
     Carver cv{mem};
     float* Rs = cv.take<float>(static_cast<size_t>(s) * d);
     float* sk32 = cv.take<float>(static_cast<size_t>(n) * kSeedRank);
     int64_t* si32 = cv.take<int64_t>(static_cast<size_t>(n) * kSeedRank);
-    float2* vlog = cv.take<float2>(static_cast<size_t>(slots) * 128 * CV);
-    int* vlog_n = cv.take<int>(static_cast<size_t>(slots) * 128);
+    float* spk = cv.take<float>(static_cast<size_t>(s_slots) * 128 * kSeedRank);
+    int64_t* spi = cv.take<int64_t>(static_cast<size_t>(s_slots) * 128 * kSeedRank);
+    float2* vlog = cv.take<float2>(static_cast<size_t>(l_slots) * 128 * CV);
+    int* vlog_n = cv.take<int>(static_cast<size_t>(l_slots) * 128);
     int* fb = cv.take<int>(static_cast<size_t>(n) + 1);
+    float* fpk = cv.take<float>(static_cast<size_t>(f_slots) * 128 * k);
+    int64_t* fpi = cv.take<int64_t>(static_cast<size_t>(f_slots) * 128 * k);
+    float* fgk = cv.take<float>(static_cast<size_t>(gmax) * 128 * k);
+    int32_t* fgi = cv.take<int32_t>(static_cast<size_t>(gmax) * 128 * k);
     {
         ProfileScope ps(stream, "exact_large_sample");
         const int64_t tot = s * d;
         gather_strided_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(dR, d, stride, s, Rs);
         KNN_LAUNCH_CHECK();
     }
-    search_device(ctx, stream, dQ, n, Rs, s, d, std::min<int64_t>(kSeedRank, s) == kSeedRank ? kSeedRank : static_cast<int>(s),
-                  metric, /*path=*/1, /*raw_keys=*/1, 0, sk32, si32, nullptr);
+    ExactArgs sa{};  // the sample search (k' = 32, raw keys, rows of Q by the list)
+    sa.Q = dQ;
+    sa.R = Rs;
+    sa.n = n;
+    sa.m = s;
+    sa.d = d;
+    sa.k = kSeedRank;
+    sa.ntiles = stiles;
+    sa.qlist = qlist;
+    sa.qcount = qcount;
+    sa.raw_keys = 1;
+    sa.out_key = sk32;
+    sa.out_idx = si32;
+    sa.part_key = spk;
+    sa.part_idx = spi;
+    launch_exact(metric, sa, stream);
     // 2. the threshold-log pass
     ExactArgs a{};
     a.Q = dQ;
@@ -257,6 +282,8 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     a.d = d;
     a.k = k;
     a.ntiles = ntiles;
+    a.qlist = qlist;
+    a.qcount = qcount;
     a.t0 = sk32 + (kSeedRank - 1);
     a.t0_stride = kSeedRank;
     a.vlog = vlog;
@@ -265,24 +292,26 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     launch_exact_log(metric, a, stream);
     // 3. select
     KNN_CUDA_CHECK(cudaMemsetAsync(fb, 0, sizeof(int), stream));
-    SelArgs sa{};
-    sa.vlog = vlog;
-    sa.vlog_n = vlog_n;
-    sa.CV = CV;
-    sa.NC = NC;
-    sa.k = k;
-    sa.n = n;
-    sa.ntiles = ntiles;
-    sa.max_ctas = max_ctas;
-    sa.t0 = a.t0;
-    sa.t0_stride = kSeedRank;
-    sa.metric = metric;
-    sa.raw_keys = raw_keys;
-    sa.index_base = index_base;
-    sa.out = d_out;
-    sa.out_idx = d_idx;
-    sa.fb_count = fb;
-    sa.fb_list = fb + 1;
+    SelArgs sl{};
+    sl.qlist = qlist;
+    sl.qcount = qcount;
+    sl.vlog = vlog;
+    sl.vlog_n = vlog_n;
+    sl.CV = CV;
+    sl.NC = NC;
+    sl.k = k;
+    sl.n = n;
+    sl.ntiles = ntiles;
+    sl.max_ctas = lmax;
+    sl.t0 = a.t0;
+    sl.t0_stride = kSeedRank;
+    sl.metric = metric;
+    sl.raw_keys = raw_keys;
+    sl.index_base = index_base;
+    sl.out = d_out;
+    sl.out_idx = d_idx;
+    sl.fb_count = fb;
+    sl.fb_list = fb + 1;
     {
         const int nt = NC <= 16 * 256 ? 256 : 512;
         const size_t smem = static_cast<size_t>(NC) * 8;
@@ -290,32 +319,34 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
         KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         ProfileScope ps(stream, "select_exact_kernel");
-        kern<<<static_cast<unsigned>(n), nt, smem, stream>>>(sa);
+        const int64_t grid = qcount ? std::min<int64_t>(n, 8 * kSmCount) : n;
+        kern<<<static_cast<unsigned>(std::max<int64_t>(1, grid)), nt, smem, stream>>>(sl);
         KNN_LAUNCH_CHECK();
     }
-    // 4. uncertified queries: the list path (host-driven, rare)
-    int fails = 0;
-    KNN_CUDA_CHECK(cudaMemcpyAsync(&fails, fb, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
-    if (fails > 0) {
-        float* gq = nullptr;
-        float* od = nullptr;
-        int64_t* oi = nullptr;
-        KNN_CUDA_CHECK(cudaMallocAsync(&gq, sizeof(float) * fails * d, stream));
-        KNN_CUDA_CHECK(cudaMallocAsync(&od, sizeof(float) * fails * k, stream));
-        KNN_CUDA_CHECK(cudaMallocAsync(&oi, sizeof(int64_t) * fails * k, stream));
-        const int64_t tq = static_cast<int64_t>(fails) * d, to = static_cast<int64_t>(fails) * k;
-        gather_list_kernel<<<static_cast<unsigned>((tq + 255) / 256), 256, 0, stream>>>(dQ, d, fb + 1, fails, gq);
-        KNN_LAUNCH_CHECK();
-        run_exact_lists(ctx, stream, gq, fails, dR, m, d, k, metric, raw_keys, index_base, od, oi);
-        scatter_list_kernel<<<static_cast<unsigned>((to + 255) / 256), 256, 0, stream>>>(od, oi, fb + 1, fails, k,
-                                                                                       d_out, d_idx);
-        KNN_LAUNCH_CHECK();
-        KNN_CUDA_CHECK(cudaFreeAsync(gq, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(od, stream));
-        KNN_CUDA_CHECK(cudaFreeAsync(oi, stream));
-    }
-    ctx.s->last_fallbacks = fails;
+    // 4. uncertified rows (a tail estimate of T0): the list path over the
+    //    device-side row list (global lists), still on the device
+    ExactArgs fa{};
+    fa.Q = dQ;
+    fa.R = dR;
+    fa.n = n;
+    fa.m = m;
+    fa.d = d;
+    fa.k = k;
+    fa.ntiles = ntiles;
+    fa.qlist = fb + 1;
+    fa.qcount = fb;
+    fa.index_base = index_base;
+    fa.raw_keys = raw_keys;
+    fa.out_key = d_out;
+    fa.out_idx = d_idx;
+    fa.part_key = fpk;
+    fa.part_idx = fpi;
+    fa.glist_key = fgk;
+    fa.glist_idx = fgi;
+    launch_exact(metric, fa, stream);
+    if (ctx.s->fb_dev)
+        KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+    ctx.s->fb_on_device = true;
     KNN_CUDA_CHECK(cudaFreeAsync(mem, stream));
 }
 

@@ -370,7 +370,18 @@ void tensor_resolve_fallbacks(DeviceContext& ctx, cudaStream_t stream, const Ten
     // On the device for every k: the exact kernel reads the failed query list
     // and its count from HBM (fixed grid), merge_exact finishes the blocks it
     // spread over several CTAs -- no host round trip, so the search stays
-    // asynchronous and graph-capturable.
+    // asynchronous and graph-capturable.  Large k on a large reference set:
+    // the exact path's threshold-log selection over the same list.
+    if (exact_large_applies(refs.m, k)) {
+        run_exact_large(ctx, stream, dQ, n, refs.dR, refs.m, refs.d, k, kL2, raw_keys, index_base, d_out,
+                        d_idx, fb + 1, fb);
+        // the count the caller reads is the tensor path's (fb), not the
+        // nested selection's
+        if (ctx.s->fb_dev)
+            KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        ctx.s->fb_on_device = true;
+        return;
+    }
     ExactArgs ea{};
     ea.Q = dQ;
     ea.R = refs.dR;
