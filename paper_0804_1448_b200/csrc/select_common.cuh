@@ -221,6 +221,86 @@ __device__ int block_exclusive_scan(int v, int* total) {
     return base;
 }
 
+// An upper bound B >= the k-th smallest of x[0..n) (at least k finite values;
+// +inf entries are ignored)
+// from ONE histogram pass: 256 linear bins over [min, hi]; B = the largest
+// value in the bins up to the one where the running count reaches k, so at
+// least k values are <= B (a valid bound, at most one bin above the exact
+// k-th).  hist: 256 shared counters; red: 2 shared words.
+__device__ float block_kth_upper_bound(const float* x, int n, int k, float hi, unsigned* hist, unsigned* red) {
+    const int t = threadIdx.x;
+    for (int b = t; b < 256; b += blockDim.x) hist[b] = 0u;
+    __shared__ unsigned s_hi;
+    if (t == 0) {
+        red[0] = 0xffffffffu;  // min (ordered bits)
+        red[1] = 0u;           // result (ordered bits)
+        s_hi = 0u;             // max finite value (ordered bits)
+    }
+    __syncthreads();
+    // the bins span the finite values only (a log may hold +inf padding
+    // references when its threshold is infinite; they never count)
+    unsigned lo_l = 0xffffffffu, hi_l = 0u;
+    for (int e = t; e < n; e += blockDim.x) {
+        const float v = x[e];
+        if (v < kInf) {
+            lo_l = min(lo_l, ord(v));
+            hi_l = max(hi_l, ord(v));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo_l = min(lo_l, __shfl_xor_sync(0xffffffffu, lo_l, o));
+        hi_l = max(hi_l, __shfl_xor_sync(0xffffffffu, hi_l, o));
+    }
+    if ((t & 31) == 0) {
+        atomicMin(red, lo_l);
+        atomicMax(&s_hi, hi_l);
+    }
+    __syncthreads();
+    const float lo = unord(red[0]);
+    const float hi_f = fminf(hi, unord(s_hi));
+    const float scale = hi_f > lo ? 256.f / (hi_f - lo) : 0.f;
+    auto bin_of = [&](float v) { return min(255, max(0, static_cast<int>((v - lo) * scale))); };
+    for (int e = t; e < n; e += blockDim.x)
+        if (x[e] < kInf) atomicAdd(hist + bin_of(x[e]), 1u);
+    __syncthreads();
+    __shared__ int s_bin;
+    if (t < 32) {  // warp 0: the bin where the running count reaches k
+        unsigned c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = hist[8 * t + j];
+            tot += c[j];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (t >= o) incl += y;
+        }
+        const unsigned excl = incl - tot;
+        if (excl < static_cast<unsigned>(k) && static_cast<unsigned>(k) <= incl) {
+            unsigned acc = excl;
+            int j = 0;
+            for (; j < 7; ++j) {
+                if (acc + c[j] >= static_cast<unsigned>(k)) break;
+                acc += c[j];
+            }
+            s_bin = 8 * t + j;
+        }
+    }
+    __syncthreads();
+    const int bk = s_bin;
+    unsigned mx = 0u;
+    for (int e = t; e < n; e += blockDim.x)
+        if (x[e] < kInf && bin_of(x[e]) <= bk) mx = max(mx, ord(x[e]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0) atomicMax(red + 1, mx);
+    __syncthreads();
+    return unord(red[1]);
+}
+
 }  // namespace
 
 }  // namespace sel

@@ -76,9 +76,9 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
             }
         }
         __syncthreads();
-        // A_(k) by radix select on the order-preserving key bits (4 x 8-bit
-        // digits, block histograms), no sort
-        const float ak = block_kth_smallest(sk, total, k, s_hist, s_sel);
+        // a bound B >= A_(k) from one histogram pass (at most one of 256 bins
+        // above A_(k): a few more candidates than thresh(A_(k)), all valid)
+        const float ak = block_kth_upper_bound(sk, total, k, T0, s_hist, reinterpret_cast<unsigned*>(s_sel));
         const Consts qc = load_consts(a.f, q);
         tau = thresh(ak, qc);
         ok = tau <= T0;  // every reference with A <= tau was logged
