@@ -37,6 +37,7 @@ struct Scratch {
     DeviceArena io;          // host-API staging of inputs / outputs
     DeviceArena refs;        // tensor path: prepared reference set of a one-shot search
     DeviceArena coll;        // multi-GPU: local and all-gathered shard lists
+    DeviceArena xl;          // exact large-k selection (also the tensor path's large-k fallback)
     int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
     int* fb_dev = nullptr;   // ... the same count, when resolved on the device
     bool fb_on_device = false;

@@ -236,9 +236,10 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     sz.take<int64_t>(static_cast<size_t>(f_slots) * 128 * k);
     sz.take<float>(static_cast<size_t>(gmax) * 128 * k);
     sz.take<int32_t>(static_cast<size_t>(gmax) * 128 * k);
-    char* mem = nullptr;
-    KNN_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&mem), sz.used + 256, stream));
-    Carver cv{mem};
+    // its own grow-only arena: the caller's search scratch (the tensor path's
+    // lists and fallback list) is live while this runs
+    ctx.s->xl.reserve(sz.used + 256);
+    Carver cv{static_cast<char*>(ctx.s->xl.base())};
     float* Rs = cv.take<float>(static_cast<size_t>(s) * d);
     float* sk32 = cv.take<float>(static_cast<size_t>(n) * kSeedRank);
     int64_t* si32 = cv.take<int64_t>(static_cast<size_t>(n) * kSeedRank);
@@ -347,7 +348,6 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     if (ctx.s->fb_dev)
         KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
     ctx.s->fb_on_device = true;
-    KNN_CUDA_CHECK(cudaFreeAsync(mem, stream));
 }
 
 }  // namespace knnb200
