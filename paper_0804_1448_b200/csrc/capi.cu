@@ -329,6 +329,32 @@ void search_staged(DeviceContext& ctx, const float* q, int64_t n, const float* r
 // search.  Coordinates are validated on the device and checked before any
 // result is returned; certification fallbacks of all chunks are collected and
 // resolved once at the end.
+// Query chunk boundaries of the pipelined host search: equal chunks of at
+// most pipe_chunk() queries, at least two, multiples of the 256-query tile
+// pair.  Dev knob KNN_B200_PIPE_CHUNKS="a,b,c": explicit leading chunk sizes
+// (rounded to 256), the rest in one chunk.
+static std::vector<int64_t> pipe_schedule(int64_t n) {
+    std::vector<int64_t> st{0};
+    if (const char* e = std::getenv("KNN_B200_PIPE_CHUNKS")) {
+        const char* p = e;
+        while (*p && st.back() < n) {
+            char* end = nullptr;
+            const long long v = std::strtoll(p, &end, 10);
+            if (end == p) break;
+            const int64_t sz = std::max<int64_t>(256, (v + 255) / 256 * 256);
+            st.push_back(std::min(n, st.back() + sz));
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (st.back() < n) st.push_back(n);
+        return st;
+    }
+    const int64_t chunks = std::max<int64_t>(2, (n + pipe_chunk() - 1) / pipe_chunk());
+    const int64_t csz = ((n + chunks - 1) / chunks + 255) / 256 * 256;
+    for (int64_t q0 = csz; q0 < n; q0 += csz) st.push_back(q0);
+    st.push_back(n);
+    return st;
+}
+
 void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float* r, int64_t m,
                       int d, int k, int raw_keys, float* out_dist, int64_t* out_idx) {
     cudaStream_t s = ctx.stream, cs = ctx.copy_stream;
@@ -373,10 +399,9 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     tensor_prep_refs(s, dR, m, d, ctx.s->refs.base(), refs);
     // chunks of <= pipe_chunk() queries, at least two (n >= pipe_chunk() here),
     // multiples of the 256-query tile pair
-    const int64_t chunks = std::max<int64_t>(2, (n + pipe_chunk() - 1) / pipe_chunk());
-    const int64_t csz = ((n + chunks - 1) / chunks + 255) / 256 * 256;
+    std::vector<int64_t> cstart = pipe_schedule(n);
     FallbackSink sink{fb, fb + 1, 0};
-    const int64_t nch = (n + csz - 1) / csz;
+    const int64_t nch = static_cast<int64_t>(cstart.size()) - 1;
     while (static_cast<int64_t>(ctx.pipe_ev.size()) < 2 * nch) {
         cudaEvent_t e;
         KNN_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -385,7 +410,7 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     // 1. every chunk's H2D, back to back on the copy stream (a chunk's D2H
     //    queued between them would hold the next copy behind a search)
     for (int64_t c = 0; c < nch; ++c) {
-        const int64_t q0 = c * csz, nq = std::min(csz, n - q0);
+        const int64_t q0 = cstart[c], nq = cstart[c + 1] - q0;
         KNN_CUDA_CHECK(cudaMemcpyAsync(dQ + q0 * d, q + q0 * d, sizeof(float) * nq * d,
                                        cudaMemcpyHostToDevice, cs));
         KNN_CUDA_CHECK(cudaEventRecord(ctx.pipe_ev[2 * c], cs));
@@ -393,7 +418,7 @@ void search_pipelined(DeviceContext& ctx, const float* q, int64_t n, const float
     // 2. per chunk: validate + search as soon as its rows landed; its D2H
     //    (copy stream, after all H2D) overlaps the next chunk's search
     for (int64_t c = 0; c < nch; ++c) {
-        const int64_t q0 = c * csz, nq = std::min(csz, n - q0);
+        const int64_t q0 = cstart[c], nq = cstart[c + 1] - q0;
         KNN_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.pipe_ev[2 * c], 0));
         finite_scan_kernel<<<scan_grid(nq * d), 256, 0, s>>>(dQ + q0 * d, nq * d, dbad, q0 * d);
         KNN_LAUNCH_CHECK();
