@@ -217,6 +217,18 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// Same, SWIZZLE_32B: rows of 32 B (a 16-element fp16 K slice), 8-row core
+// groups 256 B apart (SBO); the narrow K tail block of the folded norms.
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;              // LBO (ignored for swizzled K-major)
+    d |= static_cast<uint64_t>(256 >> 4) << 32;       // SBO
+    d |= static_cast<uint64_t>(1) << 46;              // version (Blackwell)
+    d |= static_cast<uint64_t>(6) << 61;              // SWIZZLE_32B
+    return d;
+}
+
 // Programmatic dependent launch: a kernel launched with the programmatic
 // stream-serialization attribute may start (prologue) while its predecessor
 // finishes; pdl_wait() blocks until the predecessor grid completed and its

@@ -38,12 +38,13 @@ __device__ __forceinline__ constexpr int kMode(const FilterArgs&) { return 0; }
 template <int KR, bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                  const __grid_constant__ CUtensorMap tqt, const __grid_constant__ CUtensorMap trt,
                   FilterArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B aligned start, derived by offset so the compiler keeps the shared
     // address space (LDS/STS instead of generic accesses)
     unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int KBB = a.KB * 16384;  // bytes of one 128-row operand tile
+    const int KBB = a.tile_bytes;  // bytes of one 128-row operand tile
     unsigned char* As = base;                // 2 query tiles
     unsigned char* Bs = base + 2 * KBB;      // stages x reference tile
     float* GB = reinterpret_cast<float*>(Bs + a.stages * KBB);        // [CAP][512] group minima
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
     const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
     if (warp == 0) {
-        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, 0);
+        if (sm100::elect_one()) producer_role(&tq, &tr, &tqt, &trt, a, P, u_begin, u_end, 0);
     } else if (warp == 1) {
         if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, 0, 0);
     } else if (warp == 3) {
@@ -302,10 +303,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1)
     filter_fixed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tr,
+                        const __grid_constant__ CUtensorMap tqt, const __grid_constant__ CUtensorMap trt,
                         FilterArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int KBB = a.KB * 16384;
+    const int KBB = a.tile_bytes;
     unsigned char* As = base;
     unsigned char* Bs = base + 2 * KBB;
     float* RN = reinterpret_cast<float*>(Bs + a.stages * KBB);  // [EPI_WARPS][128] staged norms
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp < 4) sm100::reg_dealloc<CTRL_REGS>();
     const Pipe P{As, Bs, KBB, full, empty, a_full, a_empty, tfull, tempty, tmem};
     if (warp == 0) {
-        if (sm100::elect_one()) producer_role(&tq, &tr, a, P, u_begin, u_end, a.W);
+        if (sm100::elect_one()) producer_role(&tq, &tr, &tqt, &trt, a, P, u_begin, u_end, a.W);
     } else if (warp == 1) {
         if (sm100::elect_one()) mma_role(a, P, u_begin, u_end, a.W, 0);
     } else if (warp == 3) {
@@ -501,13 +503,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace
 
-void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
-                   int G, size_t smem, cudaStream_t stream) {
+void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const CUtensorMap& tqt,
+                   const CUtensorMap& trt, const FilterArgs& fa, int G, size_t smem, cudaStream_t stream) {
     auto go = [&](auto kern) {
         KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         ProfileScope ps(stream, "tc_filter_kernel");
-        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
+        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, tqt, trt, fa));
     };
 #define KNN_F(KRV) \
     if (fa.fold) go(filter_kernel<KRV, true>); else go(filter_kernel<KRV, false>)
@@ -524,14 +526,15 @@ void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const F
     KNN_LAUNCH_CHECK();
 }
 
-void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
-                         int G, size_t smem, cudaStream_t stream) {
+void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const CUtensorMap& tqt,
+                         const CUtensorMap& trt, const FilterArgs& fa, int G, size_t smem,
+                         cudaStream_t stream) {
     auto kern = fa.fold ? filter_fixed_kernel<true> : filter_fixed_kernel<false>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {
         ProfileScope ps(stream, "tc_filter_fixed_kernel");
-        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, fa));
+        KNN_CUDA_CHECK(launch_kernel(kern, G, THREADS, smem, stream, pdl_enabled(1), tq, tr, tqt, trt, fa));
     }
     KNN_LAUNCH_CHECK();
 }

@@ -99,7 +99,9 @@ struct FilterArgs {
     int64_t U;             // pairs * rtiles work units (one 128-reference tile x 256 queries)
     int G;                 // CTAs
     int S_max;             // partial-list slots per query tile
-    int KB;                // 64-wide K blocks
+    int KB;                // 64-wide K blocks (full)
+    int tail;              // 1: a narrow 16-wide K block follows (SWIZZLE_32B)
+    int tile_bytes;        // bytes of one 128-row operand tile in shared memory
     int nslices;           // K / 16 MMA slices
     int stages;
     int k, Kq;
@@ -371,10 +373,15 @@ struct Pipe {  // one filter CTA's pipeline objects
 // warp 0, one elected thread: TMA loads of the query-tile pair (once per
 // segment) and of every unit's reference tile into the stage ring
 __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUtensorMap* tr,
+                                              const CUtensorMap* tqt, const CUtensorMap* trt,
                                               const FilterArgs& a, const Pipe& P, int64_t ub,
                                               int64_t ue, int W) {
     sm100::tma_prefetch(tq);
     sm100::tma_prefetch(tr);
+    if (a.tail) {
+        sm100::tma_prefetch(tqt);
+        sm100::tma_prefetch(trt);
+    }
     int stage = 0;
     uint32_t phase = 0, a_par = 0;
     int cur_p = -1;
@@ -387,10 +394,14 @@ __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUten
                 a_par ^= 1u;
             }
             sm100::mbar_expect_tx(P.a_full, static_cast<uint32_t>(2 * P.KBB));
-            for (int g = 0; g < 2; ++g)
+            for (int g = 0; g < 2; ++g) {
                 for (int kb = 0; kb < a.KB; ++kb)
                     sm100::tma_load_2d(P.As + g * P.KBB + kb * 16384, tq, P.a_full, kb * 64,
                                        (2 * sq.p + g) * TILE);
+                if (a.tail)
+                    sm100::tma_load_2d(P.As + g * P.KBB + a.KB * 16384, tqt, P.a_full, 0,
+                                       (2 * sq.p + g) * TILE);
+            }
             cur_p = sq.p;
         }
         sm100::mbar_wait_sleep(P.empty + stage, phase ^ 1u);
@@ -399,6 +410,7 @@ __device__ __forceinline__ void producer_role(const CUtensorMap* tq, const CUten
         const int rt = sq.tile();
         for (int kb = 0; kb < a.KB; ++kb)
             sm100::tma_load_2d(dst + kb * 16384, tr, P.full + stage, kb * 64, rt * TILE);
+        if (a.tail) sm100::tma_load_2d(dst + a.KB * 16384, trt, P.full + stage, 0, rt * TILE);
         if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
@@ -443,10 +455,16 @@ __device__ __forceinline__ void mma_role(const FilterArgs& a, const Pipe& P, int
             sm100::tc_fence_after();
             const uint32_t a0 = sm100::smem_u32(P.As + g * P.KBB);
             const uint32_t dt = P.tmem + static_cast<uint32_t>((2 * g + b) * TILE);
-            for (int ks = 0; ks < a.nslices; ++ks) {
+            const int main_slices = a.tail ? a.nslices - 1 : a.nslices;
+            for (int ks = 0; ks < main_slices; ++ks) {
                 const uint32_t off = static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32);
                 sm100::mma_f16_ss(dt, sm100::sdesc_k_sw128(a0 + off), sm100::sdesc_k_sw128(b0 + off),
                                   idesc, ks > 0 ? 1u : 0u);
+            }
+            if (a.tail) {  // the 16-wide folded-norm K block
+                const uint32_t off = static_cast<uint32_t>(a.KB * 16384);
+                sm100::mma_f16_ss(dt, sm100::sdesc_k_sw32(a0 + off), sm100::sdesc_k_sw32(b0 + off), idesc,
+                                  main_slices > 0 ? 1u : 0u);
             }
             sm100::mma_commit(P.tfull + 2 * g + b);
         }
@@ -498,6 +516,8 @@ __host__ __device__ constexpr size_t rr_warp_bytes(int span, int k) {
 struct Layout {
     int d16, Kp, KB, norm_col, stages, Kq;
     bool fold;
+    bool tail;        // fold with a narrow 16-wide K block (d16 a multiple of 64)
+    int tile_bytes;   // shared-memory bytes of one 128-row operand tile
     size_t smem;
 };
 
@@ -530,24 +550,32 @@ inline Layout layout_for(int d, int k) {
     const size_t epi = static_cast<size_t>(EPI_THREADS) * CAP * 4 +
                        static_cast<size_t>(EPI_WARPS) * TILE * 4;
     const size_t fixed = epi + 1024 /*align*/ + 512 /*barriers*/;
-    auto stages_for = [&](int KB) {
-        const size_t per = static_cast<size_t>(KB) * 16384;
+    auto stages_for = [&](size_t per) {
         const long avail = static_cast<long>(SMEM_LIMIT) - static_cast<long>(fixed + 2 * per);
         return avail > 0 ? static_cast<int>(avail / static_cast<long>(per)) : 0;
     };
-    if (kb_fold == kb_plain || stages_for(kb_fold) >= 3) {
+    // folded norms past a multiple of 64 columns: a narrow 16-wide K block
+    // (SWIZZLE_32B) instead of a mostly empty 64-wide one
+    const bool tail = kfold % 64 == 16;
+    const size_t per_fold = tail ? static_cast<size_t>(kfold / 64) * 16384 + 4096
+                                 : static_cast<size_t>(kb_fold) * 16384;
+    if (kb_fold == kb_plain || stages_for(per_fold) >= 3) {
         L.fold = true;
+        L.tail = tail;
         L.Kp = kfold;
-        L.KB = kb_fold;
+        L.KB = tail ? kfold / 64 : kb_fold;
         L.norm_col = ncol;
+        L.tile_bytes = static_cast<int>(per_fold);
     } else {
         L.fold = false;
+        L.tail = false;
         L.Kp = L.d16;
         L.KB = kb_plain;
         L.norm_col = -1;
+        L.tile_bytes = kb_plain * 16384;
     }
-    L.stages = std::min(stages_for(L.KB), 6);
-    L.smem = fixed + static_cast<size_t>(L.KB) * 16384 * (2 + L.stages);
+    L.stages = std::min(stages_for(static_cast<size_t>(L.tile_bytes)), 6);
+    L.smem = fixed + static_cast<size_t>(L.tile_bytes) * (2 + L.stages);
     return L;
 }
 
@@ -557,10 +585,11 @@ void launch_range(const float* X, int64_t rows, int d, unsigned* mn, unsigned* m
 void launch_scale(const unsigned* mn, const unsigned* mx, int d, int Kp, float* mu, float* scale,
                   unsigned* gmax, cudaStream_t stream);
 void launch_convert(const PrepArgs& pr, bool query, cudaStream_t stream);
-void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
-                   int G, size_t smem, cudaStream_t stream);
-void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const FilterArgs& fa,
-                         int G, size_t smem, cudaStream_t stream);
+void launch_filter(int Kq, const CUtensorMap& tq, const CUtensorMap& tr, const CUtensorMap& tqt,
+                   const CUtensorMap& trt, const FilterArgs& fa, int G, size_t smem, cudaStream_t stream);
+void launch_filter_fixed(const CUtensorMap& tq, const CUtensorMap& tr, const CUtensorMap& tqt,
+                         const CUtensorMap& trt, const FilterArgs& fa, int G, size_t smem,
+                         cudaStream_t stream);
 void launch_select_large(const LargeArgs& la, cudaStream_t stream);
 void launch_rerank(const RerankArgs& ra, size_t smem, cudaStream_t stream);
 }  // namespace tp

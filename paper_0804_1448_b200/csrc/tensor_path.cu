@@ -232,6 +232,8 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     fa.G = G;
     fa.S_max = S_max;
     fa.KB = L.KB;
+    fa.tail = L.tail ? 1 : 0;
+    fa.tile_bytes = L.tile_bytes;
     fa.nslices = L.Kp / 16;
     fa.stages = L.stages;
     fa.k = k;
@@ -266,6 +268,9 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     }
     const CUtensorMap tq = make_tmap_f16_sw128(Qh, n_pad, L.Kp, TILE, 64);
     const CUtensorMap tr = make_tmap_f16_sw128(Rh, m_pad, L.Kp, TILE, 64);
+    // the narrow folded-norm K block (unused maps repeat the main ones)
+    const CUtensorMap tqt = L.tail ? make_tmap_f16_tail16(Qh, n_pad, L.Kp, L.KB * 64, TILE) : tq;
+    const CUtensorMap trt = L.tail ? make_tmap_f16_tail16(Rh, m_pad, L.Kp, L.KB * 64, TILE) : tr;
     if (large) {
         // seed: W tiles whose 32nd smallest group minimum estimates the
         // (margin*k)-th smallest A (rank ~ m * 32 / (128 W)), W >= 2
@@ -280,13 +285,13 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         int stages_fixed = std::min(L.stages + 2, 6);
         auto fixed_bytes = [&](int st) {
             return 1024 + 512 + static_cast<size_t>(EPI_WARPS) * TILE * 4 +
-                   static_cast<size_t>(L.KB) * 16384 * (2 + st);
+                   static_cast<size_t>(L.tile_bytes) * (2 + st);
         };
         while (stages_fixed > 2 && fixed_bytes(stages_fixed) > static_cast<size_t>(SMEM_LIMIT))
             --stages_fixed;
         const size_t smem_fixed = fixed_bytes(stages_fixed);
         fa.stages = stages_fixed;
-        launch_filter_fixed(tq, tr, fa, G, smem_fixed, stream);
+        launch_filter_fixed(tq, tr, tqt, trt, fa, G, smem_fixed, stream);
         LargeArgs la{};
         la.Q = dQ;
         la.R = dR;
@@ -308,7 +313,7 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         la.fb_offset = sink ? sink->offset : 0;
         launch_select_large(la, stream);
     } else {
-    launch_filter(L.Kq, tq, tr, fa, G, L.smem, stream);
+    launch_filter(L.Kq, tq, tr, tqt, trt, fa, G, L.smem, stream);
     if (want_stats) {
         unsigned long long h[8];
         KNN_CUDA_CHECK(cudaMemcpyAsync(h, fa.stats, sizeof(h), cudaMemcpyDeviceToHost, stream));

@@ -45,4 +45,20 @@ CUtensorMap make_tmap_f16_sw128(const void* base, uint64_t rows, uint64_t cols,
     return m;
 }
 
+CUtensorMap make_tmap_f16_tail16(const void* base, uint64_t rows, uint64_t pitch, uint64_t col0,
+                                 uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {16, rows};
+    cuuint64_t strides[1] = {pitch * 2};
+    cuuint32_t box[2] = {16, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    void* p = const_cast<char*>(static_cast<const char*>(base) + col0 * 2);
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, p, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled (tail) failed with CUresult " + std::to_string(r));
+    return m;
+}
+
 }  // namespace knnb200
