@@ -500,6 +500,33 @@ def run_line(be, plumb, letter, cfg, args, world, rank, path):
     if comm is not None:
         comm.close()
     index.close()
+    # N > 1: the same workload on this one GPU (all of R), so the line carries
+    # its own single-GPU baseline for the scaling ratio (BENCH's N = 1 line is
+    # the config-B headline, a different workload)
+    single = None
+    if world > 1 and rank == 0:
+        Rf = be.empty((m, d))
+        be.fill_uniform(Rf, sr, 0)
+        ixf = be.index(Rf, m, d, 0)
+        be.search(ixf, Q, n, k, od, oi, path)
+        be.sync()
+        reps = max(2, min(args.steps, 5))
+        s2 = [be.event() for _ in range(reps)]
+        e2 = [be.event() for _ in range(reps)]
+        for i in range(reps):
+            be.flush_l2()
+            be.record(s2[i])
+            be.search(ixf, Q, n, k, od, oi, path)
+            be.record(e2[i])
+        be.sync()
+        ms2 = sum(be.elapsed_ms(a, b) for a, b in zip(s2, e2)) / reps
+        ixf.close()
+        del Rf
+        single = {"n_gpus": 1, "value": round(n / (ms2 / 1e3), 1), "unit": "queries/s",
+                  "ms_per_step": round(ms2, 5), "steps": reps,
+                  "ratio": round(value / (n / (ms2 / 1e3)), 3),
+                  "note": "rank 0 alone, all of R on its GPU, same index search; "
+                          "ratio = this line's value / this value"}
     if rank != 0:
         return None
     return {
@@ -521,6 +548,7 @@ def run_line(be, plumb, letter, cfg, args, world, rank, path):
                    "vs_baseline_ref": "paper Table 1 BF-CUDA 8800 GTX, 878 q/s" if letter == "B"
                    else "no published number for this config"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "device_one_shot": oneshot,
+        "single_gpu_same_workload": single,
         "gpu_launches": launches,
         "correctness_gate": gate, "clocks": clocks.summary(),
     }
