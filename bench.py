@@ -504,7 +504,7 @@ def run_line(be, plumb, letter, cfg, args, world, rank, path):
     # its own single-GPU baseline for the scaling ratio (BENCH's N = 1 line is
     # the config-B headline, a different workload)
     single = None
-    if world > 1 and rank == 0:
+    if (world > 1 or os.environ.get("KNN_BENCH_FORCE_SINGLE")) and rank == 0:  # env: dev check on 1 GPU
         Rf = be.empty((m, d))
         be.fill_uniform(Rf, sr, 0)
         ixf = be.index(Rf, m, d, 0)
