@@ -200,10 +200,45 @@ bool exact_large_applies(int64_t m, int k) {
     return k > static_cast<int>(exact_smem_list_limit_k()) && k <= 1024 && m >= 4096;
 }
 
+namespace {
+__global__ void add_count_kernel(int* acc, const int* src, bool first) {
+    if (threadIdx.x == 0) *acc = (first ? 0 : *acc) + *src;
+}
+}  // namespace
+
+static void run_exact_large_chunk(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                                  const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                                  int64_t index_base, float* d_out, int64_t* d_idx, const int* qlist,
+                                  const int* qcount, int* fb_total, bool first);
+
+// A host-known query set is processed in chunks of at most kChunk queries: the
+// logs take (G + n / 128) x 128 x CV entries, so chunking bounds the scratch
+// (k = 1024: ~3.6 GB per chunk).  A device-side list is one chunk (the tensor
+// path's fallback list; its capacity is the search's own query count).
+constexpr int64_t kChunk = 32768;
+
 void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
                      const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
                      int64_t index_base, float* d_out, int64_t* d_idx, const int* qlist,
                      const int* qcount) {
+    if (qlist || n <= kChunk) {
+        run_exact_large_chunk(ctx, stream, dQ, n, dR, m, d, k, metric, raw_keys, index_base, d_out, d_idx,
+                              qlist, qcount, nullptr, true);
+        return;
+    }
+    int* total = ctx.s->fb_dev;  // the fallback count over all chunks
+    for (int64_t q0 = 0; q0 < n; q0 += kChunk) {
+        const int64_t nq = std::min(kChunk, n - q0);
+        run_exact_large_chunk(ctx, stream, dQ + q0 * d, nq, dR, m, d, k, metric, raw_keys, index_base,
+                              d_out + q0 * k, d_idx + q0 * k, nullptr, nullptr, total, q0 == 0);
+    }
+    ctx.s->fb_on_device = total != nullptr;
+}
+
+static void run_exact_large_chunk(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int64_t n,
+                                  const float* dR, int64_t m, int d, int k, int metric, int raw_keys,
+                                  int64_t index_base, float* d_out, int64_t* d_idx, const int* qlist,
+                                  const int* qcount, int* fb_total, bool first) {
     // Everything below is stream-ordered device work: no host round trip, so
     // the search is asynchronous and graph-capturable; with (qlist, qcount)
     // it serves a device-side query list (the tensor path's certification
@@ -345,6 +380,11 @@ void run_exact_large(DeviceContext& ctx, cudaStream_t stream, const float* dQ, i
     fa.glist_key = fgk;
     fa.glist_idx = fgi;
     launch_exact(metric, fa, stream);
+    if (fb_total) {  // chunked: accumulate the chunk's count
+        add_count_kernel<<<1, 32, 0, stream>>>(fb_total, fb, first);
+        KNN_LAUNCH_CHECK();
+        return;
+    }
     if (ctx.s->fb_dev)
         KNN_CUDA_CHECK(cudaMemcpyAsync(ctx.s->fb_dev, fb, sizeof(int), cudaMemcpyDeviceToDevice, stream));
     ctx.s->fb_on_device = true;

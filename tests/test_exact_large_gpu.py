@@ -97,3 +97,17 @@ def test_large_k_unrepresentative_sample_falls_back(knn, oracle):
         ri, rd = oracle.knn(Q, R, k, metric)
         rep = compare(t.index, t.distance, ri, rd, Q, R, metric, oracle=oracle)
         assert rep.ok, str(rep)
+
+
+def test_large_k_query_chunks(knn, oracle):
+    """More than one 32768-query chunk: every chunk's rows land in place, the
+    fallback count sums over the chunks."""
+    n, m, d, k = 33000, 4096, 8, 150
+    Q = oracle.uniform_f32(n, d, 931)
+    R = oracle.uniform_f32(m, d, 932)
+    t = exact(knn, Q, R, k, MANHATTAN)
+    assert knn.last_fallback_count() == 0
+    rows = np.r_[0:40, 32750:32800, n - 40:n]
+    ri, rd = oracle.knn(Q[rows], R, k, MANHATTAN)
+    rep = compare(t.index[rows], t.distance[rows], ri, rd, Q[rows], R, MANHATTAN, oracle=oracle)
+    assert rep.ok, str(rep)
