@@ -152,11 +152,13 @@ def test_sphere_near_ties_are_exact(knn, oracle, spread):
     _check_exact(knn, oracle, Q, R, k)
 
 
-def test_dense_near_ties_near_fp16_range(knn, oracle):
+@pytest.mark.parametrize("d", [24, 64, 128])
+def test_dense_near_ties_near_fp16_range(knn, oracle, d):
     """Coordinates spanning the fp16 range after centring/scaling, with
-    clusters of references that tie to within an ulp."""
-    rng = np.random.default_rng(11)
-    d, k = 24, 16
+    clusters of references that tie to within an ulp (d = 64, 128: the folded
+    norms in the narrow 16-wide K block)."""
+    rng = np.random.default_rng(11 + d)
+    k = 16
     base = rng.uniform(-3e4, 3e4, (400, d)).astype(np.float32)
     R = np.repeat(base, 25, axis=0)
     R += np.float32(1.0) * rng.integers(-1, 2, R.shape).astype(np.float32)
@@ -164,13 +166,14 @@ def test_dense_near_ties_near_fp16_range(knn, oracle):
     _check_exact(knn, oracle, Q, R, k)
 
 
-def test_queries_far_outside_the_reference_range(knn, oracle):
+@pytest.mark.parametrize("d", [16, 128])
+def test_queries_far_outside_the_reference_range(knn, oracle, d):
     """a query 4096-8188 reference half-ranges away in two
     coordinates (opposite directions): its scaled coordinate t still rounds to a
     finite fp16 h, but the MMA operand -2 h overflows.  The query must be
     recomputed exactly, never certified on an infinite operand."""
     rng = np.random.default_rng(5)
-    d, m, n, k = 16, 4096, 256, 10
+    m, n, k = 4096, 256, 10
     R = rng.uniform(-1, 1, (m, d)).astype(np.float32)
     Q = rng.uniform(-1, 1, (n, d)).astype(np.float32)
     Q[::3, 0] = 6000.0
