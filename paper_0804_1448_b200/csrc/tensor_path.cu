@@ -314,18 +314,6 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         launch_select_large(la, stream);
     } else {
     launch_filter(L.Kq, tq, tr, tqt, trt, fa, G, L.smem, stream);
-    if (want_stats) {
-        unsigned long long h[8];
-        KNN_CUDA_CHECK(cudaMemcpyAsync(h, fa.stats, sizeof(h), cudaMemcpyDeviceToHost, stream));
-        KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
-        KNN_CUDA_CHECK(cudaFree(fa.stats));
-        const double warps = static_cast<double>(G) * EPI_WARPS;
-        std::fprintf(stderr,
-                     "[filter stats] per warp: tiles %.1f groups-pushed/lane %.1f drains %.1f insert-rounds "
-                     "%.1f | logged-groups/lane %.2f | kcycles/warp: drain %.1f tfull-wait %.1f total %.1f\n",
-                     h[4] / warps, h[0] / (warps * 32.0), h[1] / warps, h[2] / warps,
-                     h[3] / (warps * 32.0), h[5] / warps / 1e3, h[6] / warps / 1e3, h[7] / warps / 1e3);
-    }
     }  // small k
 
     // 3. exact re-rank (small k; large k selected above)
@@ -348,6 +336,17 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     ra.fb_offset = sink ? sink->offset : 0;
     const size_t rr_smem = static_cast<size_t>(RR_WARPS) * rr_warp_bytes(S_max * L.Kq, k);
     if (!large) launch_rerank(ra, rr_smem, stream);
+    if (want_stats) {  // dev (make EXTRA=-DKNN_B200_FILTER_STATS): re-rank candidate counts
+        unsigned long long h[8];
+        KNN_CUDA_CHECK(cudaMemcpyAsync(h, fa.stats, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        KNN_CUDA_CHECK(cudaStreamSynchronize(stream));
+        KNN_CUDA_CHECK(cudaFree(fa.stats));
+        const double qn = std::max(1.0, static_cast<double>(h[2]));
+        std::fprintf(stderr,
+                     "[rerank stats] certified queries %.0f: candidates/query %.2f, in-tau groups/query "
+                     "%.2f, logged groups/query %.2f, parts/query %.2f\n",
+                     qn, h[0] / qn, h[1] / qn, h[3] / qn, h[4] / qn);
+    }
 
     // 4. certification fallback (exact kernel on the failed queries), unless
     //    the caller collects them across several searches.

@@ -224,6 +224,13 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
             }
         }
         ok = ok && nc <= RR_CAND && nc >= k;  // heavy ties beyond the fast path: exact kernel
+        if (kStats && a.f.stats && ok && lane == 0) {
+            atomicAdd(a.f.stats + 0, static_cast<unsigned long long>(nc));
+            atomicAdd(a.f.stats + 1, static_cast<unsigned long long>(ng));
+            atomicAdd(a.f.stats + 2, 1ull);
+            atomicAdd(a.f.stats + 3, static_cast<unsigned long long>(NT));
+            atomicAdd(a.f.stats + 4, static_cast<unsigned long long>(nslots));
+        }
     }
     if (!ok) {
         if (lane == 0) {
