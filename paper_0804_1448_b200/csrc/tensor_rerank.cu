@@ -11,6 +11,7 @@
 #include "profile.cuh"
 #include "sm100.cuh"
 #include "tensor_internal.cuh"
+#include "select_common.cuh"
 #include "warp_list.cuh"
 
 namespace knnb200 {
@@ -75,11 +76,38 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         if (lane >= o) cincl += y;
     }
     const int L = __shfl_sync(0xffffffffu, cincl, 31);
-    for (int p = 0; p < nslots; ++p) {  // a list holds <= Kq <= 32 entries
-        const int cp = __shfl_sync(0xffffffffu, cnt, p);
-        const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
-        if (lane < cp)
-            sv[ep + lane] = p < 2 ? pa[p] : a.f.part_A[((p0 + p) * TILE + row) * Kq + lane];
+    if (nslots <= 2) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int cp = __shfl_sync(0xffffffffu, cnt, p);
+            const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+            if (p < nslots && lane < cp) sv[ep + lane] = pa[p];
+        }
+    } else {
+        // many parts (short stream-K parts: small query sets, long reference
+        // sets): 8 lists' loads in flight per round trip, not one
+        for (int pb = 2; pb < nslots; pb += 8) {
+            float v8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int p = pb + u;
+                const int cp = __shfl_sync(0xffffffffu, cnt, p & 31);
+                v8[u] = (p < nslots && lane < cp) ? a.f.part_A[((p0 + p) * TILE + row) * Kq + lane] : kInf;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int p = pb + u;
+                const int cp = __shfl_sync(0xffffffffu, cnt, p & 31);
+                const int ep = __shfl_sync(0xffffffffu, cincl, p & 31) - cp;
+                if (p < nslots && lane < cp) sv[ep + lane] = v8[u];
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int cp = __shfl_sync(0xffffffffu, cnt, p);
+            const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
+            if (lane < cp) sv[ep + lane] = pa[p];
+        }
     }
     __syncwarp();
 
@@ -104,31 +132,29 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
     } else if (L >= k) {
-        for (int x0 = 0; x0 < L; x0 += 32) {  // warp-uniform trip count (shuffles inside)
-            const int x = x0 + lane;
-            const bool valid = x < L;
-            const float v = valid ? sv[x] : kInf;
-            int px = 0;
-            for (int p = 1; p < nslots; ++p)
-                if (x >= __shfl_sync(0xffffffffu, cincl, p - 1)) px = p;
-            int rank = 0;
-            for (int p = 0; p < nslots; ++p) {
-                const int cp = __shfl_sync(0xffffffffu, cnt, p);
-                const int ep = __shfl_sync(0xffffffffu, cincl, p) - cp;
-                // first entry of list p that is not "less" than (v, x)
-                int lo = 0, hi = (p == px || !valid) ? 0 : cp;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    const float w = sv[ep + mid];
-                    if (p < px ? w <= v : w < v) lo = mid + 1;
-                    else hi = mid;
-                }
-                rank += p == px ? x - ep : lo;
+        // More lists: bisection on the value.  Lane p counts the entries <= v
+        // of its sorted list (binary search), the warp sums; the smallest v
+        // (in float order) with count >= k is the k-th smallest entry.
+        const int cp = lane < nslots ? cnt : 0;
+        const int ep = cincl - cnt;
+        unsigned lo = cp > 0 ? sel::ord(sv[ep]) : 0xffffffffu;
+        unsigned hi = cp > 0 ? sel::ord(sv[ep + cp - 1]) : 0u;
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        while (lo < hi) {  // warp-uniform
+            const unsigned mid = lo + ((hi - lo) >> 1);
+            const float v = sel::unord(mid);
+            int a0 = 0, a1 = cp;  // entries of list `lane` that are <= v
+            while (a0 < a1) {
+                const int md = (a0 + a1) >> 1;
+                if (sv[ep + md] <= v) a0 = md + 1;
+                else a1 = md;
             }
-            if (valid && rank == k - 1) B = v;
+            const int c = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(a0)));
+            if (c >= k) hi = mid;
+            else lo = mid + 1;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
+        B = sel::unord(lo);
     }
     const float tau = thresh(B, qc);
 
@@ -170,14 +196,14 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
                 hs[e] = 0;
                 hc[e] = 0;
                 if (t < NT) {
-                    int p = 0, ex = 0;
-                    for (int pp = 0; pp + 1 < nslots; ++pp) {
-                        const int pe = pend[pp];
-                        if (t >= pe) {
-                            p = pp + 1;
-                            ex = pe;
-                        }
+                    // part of flat head t: the first part whose end exceeds t
+                    int p = 0, b1 = nslots - 1;
+                    while (p < b1) {
+                        const int md = (p + b1) >> 1;
+                        if (pend[md] <= t) p = md + 1;
+                        else b1 = md;
                     }
+                    const int ex = p > 0 ? pend[p - 1] : 0;
                     // part-relative handle (part << 16 | slot, CG <= 4096): the global
                     // slot needs 64 bits once parts * 128 * CG >= 2^31
                     hs[e] = (p << 16) | (t - ex);
