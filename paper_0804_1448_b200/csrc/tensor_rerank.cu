@@ -19,8 +19,13 @@ namespace tp {
 
 namespace {
 
+#ifndef KNN_RR_MERGE_MAX
+#define KNN_RR_MERGE_MAX 16  // up to this many part lists: pairwise merges, more: bisection
+#endif
+
 // Warp per query.  (1) A_bound = k-th smallest of the union of the parts'
-// bound lists (rank counting over the compacted lists); tau = thresh(A_bound).
+// bound lists (merge-path split over two lists, pairwise merges up to
+// KNN_RR_MERGE_MAX lists, value bisection beyond); tau = thresh(A_bound).
 // (2) Certificate: no part's group log overflowed, so every reference with
 // A <= tau is in a log (every filter bound was >= tau).  (3) Candidates =
 // logged values <= tau; their exact FP32 keys (key_step<kL2>, bitwise the
@@ -131,6 +136,33 @@ __global__ void __launch_bounds__(RR_WARPS * 32) rerank_kernel(RerankArgs a) {
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) B = fminf(B, __shfl_xor_sync(0xffffffffu, B, o));
+    } else if (L >= k && nslots <= KNN_RR_MERGE_MAX) {
+        // A few lists: merge them one at a time, keeping the k smallest (lane t
+        // places output t by a merge-path binary search); B = the k-th.
+        const float* A = sv;
+        int na = min(k, __shfl_sync(0xffffffffu, cnt, 0));
+        float* dst = ck;
+        for (int p = 1; p < nslots; ++p) {
+            const int nb = __shfl_sync(0xffffffffu, cnt, p);
+            const float* Bl = sv + __shfl_sync(0xffffffffu, cincl, p) - nb;
+            const int out = min(k, na + nb);
+            if (lane < out) {
+                const int t = lane;
+                int lo = max(0, t - nb), hi = min(t, na);  // A entries among the first t outputs
+                while (lo < hi) {
+                    const int md = (lo + hi) >> 1;
+                    if (A[md] <= Bl[t - 1 - md]) lo = md + 1;
+                    else hi = md;
+                }
+                const int j = t - lo;
+                dst[t] = (lo < na && (j >= nb || A[lo] <= Bl[j])) ? A[lo] : Bl[j];
+            }
+            __syncwarp();
+            A = dst;
+            na = out;
+            dst = dst == ck ? ck + 32 : ck;
+        }
+        B = A[k - 1];
     } else if (L >= k) {
         // More lists: bisection on the value.  Lane p counts the entries <= v
         // of its sorted list (binary search), the warp sums; the smallest v
