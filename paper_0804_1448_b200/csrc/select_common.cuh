@@ -301,6 +301,98 @@ __device__ float block_kth_upper_bound(const float* x, int n, int k, float hi, u
     return unord(red[1]);
 }
 
+// The k smallest of n (key, index) pairs in (key, index) order by a bucket
+// sort: nb (power of two) linear bins over [min, max] of the keys (bin_of is
+// monotone in the key, so bin order is key order), a count pass, a prefix
+// sum, a scatter of the entries of the bins up to the one where the count
+// reaches k, and one thread per bin ordering its few entries by insertion.
+// O(n) work and seven barriers where the bitonic network needs n log^2 n and
+// dozens.  Writes ok/oi[0..k) and returns true; returns false (nothing
+// usable written) when the keys do not spread -- a bin up to the k-th holding
+// more than 32 entries (dense ties), equal or non-finite extremes -- and the
+// caller sorts instead.  cnt: nb shared counters; red: 3 shared words.
+template <int NT>
+__device__ bool block_bucket_topk(const float* key, const int* idx, int n, int k, float* ok, int* oi,
+                                  unsigned* cnt, int nb, unsigned* red) {
+    const int t = threadIdx.x;
+    for (int b = t; b < nb; b += NT) cnt[b] = 0u;
+    if (t == 0) {
+        red[0] = 0xffffffffu;  // min (ordered bits)
+        red[1] = 0u;           // max (ordered bits)
+        red[2] = 0u;           // [bk << 1 | dense]
+    }
+    unsigned lo_l = 0xffffffffu, hi_l = 0u;
+    for (int e = t; e < n; e += NT) {
+        const unsigned u = ord(key[e]);
+        lo_l = min(lo_l, u);
+        hi_l = max(hi_l, u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo_l = min(lo_l, __shfl_xor_sync(0xffffffffu, lo_l, o));
+        hi_l = max(hi_l, __shfl_xor_sync(0xffffffffu, hi_l, o));
+    }
+    __syncthreads();  // red / cnt initialised
+    if ((t & 31) == 0) {
+        atomicMin(red, lo_l);
+        atomicMax(red + 1, hi_l);
+    }
+    __syncthreads();
+    const float lo = unord(red[0]), hi = unord(red[1]);
+    const float scale = static_cast<float>(nb) / (hi - lo);
+    if (!(hi > lo) || !(scale < kInf) || !(hi < kInf)) return false;  // block-uniform
+    auto bin_of = [&](float v) { return min(nb - 1, static_cast<int>((v - lo) * scale)); };
+    for (int e = t; e < n; e += NT) atomicAdd(cnt + bin_of(key[e]), 1u);
+    __syncthreads();
+    // counts -> starts; thread t owns bins [t per, t per + per)
+    const int per = (nb + NT - 1) / NT;
+    const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
+    int own = 0;
+    for (int b = b0; b < b1; ++b) own += static_cast<int>(cnt[b]);
+    int total = 0;
+    int run = block_exclusive_scan<NT>(own, &total);
+    unsigned flag = 0u;
+    for (int b = b0; b < b1; ++b) {
+        const int c = static_cast<int>(cnt[b]);
+        if (run < k && c > 32) flag = 1u;
+        if (run < k && k <= run + c) flag |= static_cast<unsigned>(b) << 1;
+        cnt[b] = static_cast<unsigned>(run);
+        run += c;
+    }
+    if (flag) atomicOr(red + 2, flag);
+    __syncthreads();
+    const unsigned rf = red[2];
+    if (rf & 1u) return false;
+    const int bk = static_cast<int>(rf >> 1);
+    for (int e = t; e < n; e += NT) {
+        const float v = key[e];
+        const int b = bin_of(v);
+        if (b <= bk) {
+            const unsigned pos = atomicAdd(cnt + b, 1u);
+            ok[pos] = v;
+            oi[pos] = idx[e];
+        }
+    }
+    __syncthreads();  // cnt[b] = end of bin b
+    for (int b = t; b <= bk; b += NT) {
+        const int s0 = b > 0 ? static_cast<int>(cnt[b - 1]) : 0, s1 = static_cast<int>(cnt[b]);
+        for (int x = s0 + 1; x < s1; ++x) {
+            const float kx = ok[x];
+            const int ix = oi[x];
+            int u = x;
+            while (u > s0 && pair_less(kx, ix, ok[u - 1], oi[u - 1])) {
+                ok[u] = ok[u - 1];
+                oi[u] = oi[u - 1];
+                --u;
+            }
+            ok[u] = kx;
+            oi[u] = ix;
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
 }  // namespace
 
 }  // namespace sel

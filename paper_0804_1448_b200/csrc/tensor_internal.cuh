@@ -27,7 +27,6 @@ constexpr int kMaxLargeK = 1024;   // k > MAX_KQ: fixed-threshold filter + block
 constexpr int MAX_KQ = 32;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per CTA
 
-constexpr int LK_THREADS = 512;  // largest selection block (large k)
 constexpr int RR_WARPS = 2;      // re-rank: warps (queries) per block
 constexpr int RR_CAND = 128;     // exact candidates per query on the fast path (more: fallback)
 

@@ -299,9 +299,10 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         la.d = d;
         la.k = k;
         la.S_max = S_max;
-        int NC = 1;
-        while (NC < 2 * margin * k) NC <<= 1;
-        NC = std::min(NC, 16 * LK_THREADS);
+        // candidate capacity: values inside thresh(B) are ~1.1 k (B at most one
+        // histogram bin above A_(k)); more -> the query takes the exact path
+        int NC = 64;
+        while (NC < k + k / 2 + 64) NC <<= 1;
         la.NC = NC;
         la.f = fa;
         la.raw_keys = raw_keys;

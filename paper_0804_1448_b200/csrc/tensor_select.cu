@@ -21,183 +21,231 @@ namespace {
 
 using namespace sel;
 
-// Large-k selection, one 256-thread block per query: gather the query's
-// logged {A, index} values, bitonic-sort them by A, A_(k) = k-th; certify
-// (>= k logged, no overflow, thresh(A_(k)) <= T0); exact FP32 keys of every
-// value <= thresh(A_(k)); bitonic sort by (key, index); top k.
+// Large-k selection, one block per query.  The query's value logs (one per
+// part slot, {A, index}) stay in global memory and are streamed (L1/L2 hits
+// after the first pass); shared memory holds only the candidates:
+//  1. a bound B >= A_(k): min / max, then a 256-bin histogram over
+//     [min, min(max, T0)], then the largest value in the bins up to the one
+//     where the running count reaches k (at most one bin above A_(k));
+//  2. certificate: >= k values logged, no log overflowed, thresh(B) <= T0
+//     (every reference with A <= tau = thresh(B) was logged);
+//  3. candidates = logged values <= tau (warp-aggregated appends, at most NCC);
+//  4. their exact FP32 keys; 5. the k smallest under the (key, index) order
+//     by a bucket sort (block_bucket_topk), or a bitonic sort of all
+//     candidates when the keys do not spread (dense ties).
+// Candidate order is irrelevant: every comparison uses (key, index).
 #ifndef KNN_DBG_LARGE
 #define KNN_DBG_LARGE 0
 #endif
 
-// NT threads per query: the fewest of 64 / 128 / 256 / 512 that hold the candidate
-// capacity NC <= 16 x NT (more resident blocks, cheaper barriers)
 template <int NT>
 __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(LargeArgs a) {  // <= 64 registers
     sm100::pdl_wait();  // the fixed filter's logs are complete
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* sk = reinterpret_cast<float*>(smem_raw);   // [NC]
-    int* si = reinterpret_cast<int*>(sk + a.NC);       // [NC]
-    __shared__ int s_off[33];
-    __shared__ int s_cnt;
-    __shared__ int s_sel[2];
+    const int NCC = a.NC;                               // candidate capacity (power of two)
+    const int k = a.k;
+    float* sk = reinterpret_cast<float*>(smem_raw);    // [NCC] candidate keys
+    int* si = reinterpret_cast<int*>(sk + NCC);         // [NCC] candidate indices
+    float* ok = reinterpret_cast<float*>(si + NCC);     // [k + 32] bucket output keys
+    int* oi = reinterpret_cast<int*>(ok + k + 32);      // [k + 32] bucket output indices
+    unsigned* cnt = reinterpret_cast<unsigned*>(oi + k + 32);  // [NCC] bucket counters
+    __shared__ int s_np[32];
+    __shared__ int s_total, s_nc, s_bin;
+    __shared__ unsigned s_red[3];
     __shared__ unsigned s_hist[256];
+    const int t = threadIdx.x, lane = t & 31;
     const int64_t q = blockIdx.x;
     const int qt = static_cast<int>(q / TILE), row = static_cast<int>(q % TILE);
     const int64_t p0 = static_cast<int64_t>(qt) * a.S_max;
-    const int k = a.k;
-    if (threadIdx.x == 0) {
-        int off = 0;
-        bool over = false;
-        const int pair = qt >> 1;  // slots written: one per CTA touching the pair
-        const int nslots = a.f.pair_slots[pair];
-        for (int p = 0; p < a.S_max; ++p) {
-            const int np = p < nslots ? a.f.log_n[(p0 + p) * TILE + row] : 0;
-            over |= np > a.f.CV;
-            s_off[p] = off;
-            off += min(np, a.f.CV);
+    const int nparts = a.f.pair_slots[qt >> 1];  // slots written: one per CTA touching the pair
+    for (int b = t; b < 256; b += NT) s_hist[b] = 0u;
+    if (t < 32) {
+        const int np = t < nparts ? a.f.log_n[(p0 + t) * TILE + row] : 0;
+        const bool over = __any_sync(0xffffffffu, np > a.f.CV);
+        const int c = min(np, a.f.CV);
+        s_np[t] = c;
+        const int tot = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(c)));
+        if (t == 0) {
+            s_total = over ? -1 : tot;
+            s_nc = 0;
+            s_red[0] = 0xffffffffu;
+            s_red[1] = 0u;
+            s_red[2] = 0u;
         }
-        s_off[a.S_max] = off;
-        s_cnt = over ? -1 : off;
     }
     __syncthreads();
-    const int total = s_cnt;
+    const int total = s_total;
     const float T0 = a.f.t0[q];
-    bool ok = total >= k && total <= a.NC;
+    auto logp = [&](int p) { return a.f.vlog + ((p0 + p) * TILE + row) * a.f.CV; };
+    bool ok_q = total >= k;
     float tau = kInf;
     int nc = 0;
-    if (ok) {
-        for (int p = 0; p < a.S_max; ++p) {
-            const int o = s_off[p], np = s_off[p + 1] - o;
-            const float2* src = a.f.vlog + ((p0 + p) * TILE + row) * a.f.CV;
-            for (int e = threadIdx.x; e < np; e += blockDim.x) {
-                const float2 r = src[e];
-                sk[o + e] = r.x;
-                si[o + e] = __float_as_int(r.y);
+    if (ok_q) {
+        // 1. the bound: extremes of the finite values (a log holds +inf padding
+        //    references when its threshold is infinite; they never count)
+        unsigned lo_l = 0xffffffffu, hi_l = 0u;
+        for (int p = 0; p < nparts; ++p) {
+            const float2* src = logp(p);
+            const int np = s_np[p];
+            for (int e = t; e < np; e += NT) {
+                const float v = __ldg(&src[e].x);
+                if (v < kInf) {
+                    lo_l = min(lo_l, ord(v));
+                    hi_l = max(hi_l, ord(v));
+                }
+            }
+        }
+        lo_l = __reduce_min_sync(0xffffffffu, lo_l);
+        hi_l = __reduce_max_sync(0xffffffffu, hi_l);
+        if (lane == 0) {
+            atomicMin(s_red, lo_l);
+            atomicMax(s_red + 1, hi_l);
+        }
+        __syncthreads();
+        const float lo = unord(s_red[0]);
+        const float hi_f = fminf(T0, unord(s_red[1]));
+        const float scale = hi_f > lo ? 256.f / (hi_f - lo) : 0.f;
+        auto bin_of = [&](float v) { return min(255, max(0, static_cast<int>((v - lo) * scale))); };
+        for (int p = 0; p < nparts; ++p) {
+            const float2* src = logp(p);
+            const int np = s_np[p];
+            for (int e = t; e < np; e += NT) {
+                const float v = __ldg(&src[e].x);
+                if (v < kInf) atomicAdd(s_hist + bin_of(v), 1u);
             }
         }
         __syncthreads();
-        // a bound B >= A_(k) from one histogram pass (at most one of 256 bins
-        // above A_(k): a few more candidates than thresh(A_(k)), all valid)
-        const float ak = block_kth_upper_bound(sk, total, k, T0, s_hist, reinterpret_cast<unsigned*>(s_sel));
+        if (t < 32) {  // warp 0: the bin where the running count reaches k
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = s_hist[8 * t + j];
+                tot += c[j];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (t >= o) incl += y;
+            }
+            const unsigned excl = incl - tot;
+            if (t == 31 && incl < static_cast<unsigned>(k)) s_bin = -1;  // fewer than k finite values
+            if (excl < static_cast<unsigned>(k) && static_cast<unsigned>(k) <= incl) {
+                unsigned acc = excl;
+                int j = 0;
+                for (; j < 7; ++j) {
+                    if (acc + c[j] >= static_cast<unsigned>(k)) break;
+                    acc += c[j];
+                }
+                s_bin = 8 * t + j;
+            }
+        }
+        __syncthreads();
+        const int bk = s_bin;
+        unsigned mx = 0u;
+        if (bk >= 0)
+            for (int p = 0; p < nparts; ++p) {
+                const float2* src = logp(p);
+                const int np = s_np[p];
+                for (int e = t; e < np; e += NT) {
+                    const float v = __ldg(&src[e].x);
+                    if (v < kInf && bin_of(v) <= bk) mx = max(mx, ord(v));
+                }
+            }
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) atomicMax(s_red + 2, mx);
+        __syncthreads();
+        // 2. certificate
         const Consts qc = load_consts(a.f, q);
-        tau = thresh(ak, qc);
-        ok = tau <= T0;  // every reference with A <= tau was logged
-        if (ok) {
-            // compact the candidates (A <= tau) to the front in log order, i.e.
-            // ascending reference index (parts in slot order, each part's log in
-            // stream order); thread t owns the contiguous range [t per, t per + per)
-            const int per = (total + NT - 1) / NT;  // <= NC / NT <= 16
-            const int e0 = min(total, static_cast<int>(threadIdx.x) * per), e1 = min(total, e0 + per);
-            int mine[16];
-            int nm = 0;
-            for (int e = e0; e < e1; ++e)
-                if (sk[e] <= tau) mine[nm++] = si[e];
-            const int base = block_exclusive_scan<NT>(nm, &nc);
-            for (int j = 0; j < nm; ++j) si[base + j] = mine[j];
+        tau = bk >= 0 ? thresh(unord(s_red[2]), qc) : kInf;
+        ok_q = tau <= T0;  // every reference with A <= tau was logged
+        if (ok_q) {
+            // 3. candidates: warp-aggregated appends (order is irrelevant)
+            for (int p = 0; p < nparts; ++p) {
+                const float2* src = logp(p);
+                const int np = s_np[p];
+                for (int e0 = 0; e0 < np; e0 += NT) {
+                    const int e = e0 + t;
+                    float2 r = make_float2(kInf, 0.f);
+                    if (e < np) r = __ldg(&src[e]);
+                    const bool in = r.x <= tau;
+                    const unsigned bal = __ballot_sync(0xffffffffu, in);
+                    int base = 0;
+                    if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                    if (in && pos < NCC) si[pos] = __float_as_int(r.y);
+                }
+            }
             __syncthreads();
+            nc = s_nc;
+            ok_q = nc >= k && nc <= NCC;
         }
     }
-    if (!ok) {
-        if (threadIdx.x == 0) {
+    if (!ok_q) {
+        if (t == 0) {
             const int slot = atomicAdd(a.fb_count, 1);
             a.fb_list[slot] = a.fb_offset + static_cast<int>(q);
             if (KNN_DBG_LARGE && slot < 8)
-                printf("[select_large] q=%lld total=%d k=%d NC=%d tau=%g T0=%g nc=%d\n",
-                       static_cast<long long>(q), total, k, a.NC, tau, T0, nc);
+                printf("[select_large] q=%lld total=%d k=%d NCC=%d tau=%g T0=%g nc=%d\n",
+                       static_cast<long long>(q), total, k, NCC, tau, T0, nc);
         }
         return;
     }
-    // exact keys of the nc candidates (their indices are si[0..nc))
+    // 4. exact keys of the nc candidates
     const float* qrow = a.Q + q * a.d;
-    for (int c = threadIdx.x; c < nc; c += blockDim.x)
-        sk[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(si[c]) * a.d, a.d);
-    // Preselection: when the candidates need a longer network than k does,
-    // keep exactly the k smallest under the (key, index) order first -- every
-    // key below the k-th smallest K, then the lowest-index entries equal to K
-    // (the array is in ascending index order) -- so the bitonic network sorts
-    // k rounded up to a power of two (k = 1024: 1024 instead of 2048 entries
-    // for the ~1.1k candidates).
-    int N2 = 32, Nk = 32;
-    while (N2 < nc) N2 <<= 1;
-    while (Nk < k) Nk <<= 1;
+    for (int c = t; c < nc; c += NT) sk[c] = exact_key_l2(qrow, a.R + static_cast<int64_t>(si[c]) * a.d, a.d);
     __syncthreads();
-    if (N2 > Nk) {
-        const float K = block_kth_smallest(sk, nc, k, s_hist, s_sel);
-        const int per = (nc + NT - 1) / NT;
-        const int e0 = min(nc, static_cast<int>(threadIdx.x) * per), e1 = min(nc, e0 + per);
-        int nl = 0, ne = 0;
-        for (int e = e0; e < e1; ++e) {
-            nl += sk[e] < K ? 1 : 0;
-            ne += sk[e] == K ? 1 : 0;
+    // 5. the k smallest: bucket sort, or (dense ties) a bitonic sort of all
+    int nbk = 32;
+    while (nbk < nc) nbk <<= 1;
+    float* rk = ok;
+    int* ri = oi;
+    if (!block_bucket_topk<NT>(sk, si, nc, k, ok, oi, cnt, nbk, s_red)) {
+        for (int e = nc + t; e < nbk; e += NT) {
+            sk[e] = kInf;
+            si[e] = 0x7fffffff;
         }
-        int tot_less = 0, tot_eq = 0;
-        block_exclusive_scan<NT>(nl, &tot_less);
-        const int eq_before = block_exclusive_scan<NT>(ne, &tot_eq);
-        const int need_eq = k - tot_less;  // >= 1 (K is the k-th smallest)
-        float mk[16];
-        int mi[16];
-        int nm = 0, eq_seen = eq_before;
-        for (int e = e0; e < e1; ++e) {
-            const float x = sk[e];
-            const bool keep = x < K || (x == K && eq_seen++ < need_eq);
-            if (keep) {
-                mk[nm] = x;
-                mi[nm] = si[e];
-                ++nm;
-            }
-        }
-        int kept = 0;
-        const int base = block_exclusive_scan<NT>(nm, &kept);  // kept == k
-        for (int j = 0; j < nm; ++j) {
-            sk[base + j] = mk[j];
-            si[base + j] = mi[j];
-        }
-        nc = kept;
-        N2 = Nk;
+        bitonic_sort_kv(sk, si, nbk);
+        rk = sk;
+        ri = si;
     }
-    for (int e = nc + threadIdx.x; e < N2; e += blockDim.x) {
-        sk[e] = kInf;
-        si[e] = 0x7fffffff;
-    }
-    bitonic_sort_kv(sk, si, N2);
     // finalize: sqrt, then equal reported distances in ascending index order
     if (!a.raw_keys) {
-        for (int t = threadIdx.x; t < k; t += blockDim.x) sk[t] = __fsqrt_rn(sk[t]);
+        for (int e = t; e < k; e += NT) rk[e] = __fsqrt_rn(rk[e]);
         __syncthreads();
-        // equal reported distances in ascending index order: each run of
-        // equal distances (keys were ascending, so runs are contiguous and
-        // short) is insertion-sorted by the thread owning its first slot
-        for (int t = threadIdx.x; t < k; t += blockDim.x) {
-            if (t > 0 && sk[t - 1] == sk[t]) continue;
-            int e = t + 1;
-            while (e < k && sk[e] == sk[t]) ++e;
-            for (int x = t + 1; x < e; ++x) {
-                const int j = si[x];
+        // each run of equal distances (keys were ascending, so runs are
+        // contiguous and short) is insertion-sorted by the thread owning its
+        // first slot
+        for (int e = t; e < k; e += NT) {
+            if (e > 0 && rk[e - 1] == rk[e]) continue;
+            int f = e + 1;
+            while (f < k && rk[f] == rk[e]) ++f;
+            for (int x = e + 1; x < f; ++x) {
+                const int j = ri[x];
                 int u = x;
-                while (u > t && si[u - 1] > j) {
-                    si[u] = si[u - 1];
+                while (u > e && ri[u - 1] > j) {
+                    ri[u] = ri[u - 1];
                     --u;
                 }
-                si[u] = j;
+                ri[u] = j;
             }
         }
         __syncthreads();
     }
-    for (int t = threadIdx.x; t < k; t += blockDim.x) {
-        a.out[q * k + t] = sk[t];
-        a.out_idx[q * k + t] = a.index_base + si[t];
+    for (int e = t; e < k; e += NT) {
+        a.out[q * k + e] = rk[e];
+        a.out_idx[q * k + e] = a.index_base + ri[e];
     }
 }
 
 }  // namespace
 
 void launch_select_large(const LargeArgs& la, cudaStream_t stream) {
-    const size_t smem = static_cast<size_t>(la.NC) * 8;
-    const int NC = la.NC;
-    const int nt = NC <= 16 * 64 ? 64 : NC <= 16 * 128 ? 128 : NC <= 16 * 256 ? 256 : LK_THREADS;
-    auto sel = nt == 64    ? select_large_kernel<64>
-               : nt == 128 ? select_large_kernel<128>
-               : nt == 256 ? select_large_kernel<256> : select_large_kernel<LK_THREADS>;
+    // candidates [NC] keys + indices, bucket output [k + 32] x 2, counters [NC]
+    const size_t smem = static_cast<size_t>(la.NC) * 12 + static_cast<size_t>(la.k + 32) * 8;
+    const int nt = la.NC <= 512 ? 64 : la.NC <= 1024 ? 128 : 256;
+    auto sel = nt == 64 ? select_large_kernel<64> : nt == 128 ? select_large_kernel<128> : select_large_kernel<256>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {
