@@ -305,14 +305,16 @@ __device__ float block_kth_upper_bound(const float* x, int n, int k, float hi, u
 // sort: nb (power of two) linear bins over [min, max] of the keys (bin_of is
 // monotone in the key, so bin order is key order), a count pass, a prefix
 // sum, a scatter of the entries of the bins up to the one where the count
-// reaches k, and one thread per bin ordering its few entries by insertion.
+// reaches k, and each entry placed by its rank among its bin's few entries.
 // O(n) work and seven barriers where the bitonic network needs n log^2 n and
-// dozens.  Writes ok/oi[0..k) and returns true; returns false (nothing
-// usable written) when the keys do not spread -- a bin up to the k-th holding
+// dozens.  On success key/idx[0..k) hold the result (ok / oi: scratch for
+// the scattered bins) and it returns true; it returns false (key / idx
+// untouched) when the keys do not spread -- a bin up to the k-th holding
 // more than 32 entries (dense ties), equal or non-finite extremes -- and the
-// caller sorts instead.  cnt: nb shared counters; red: 3 shared words.
+// caller sorts instead.  cnt: nb shared counters (16-byte aligned); red: 3
+// shared words.
 template <int NT>
-__device__ bool block_bucket_topk(const float* key, const int* idx, int n, int k, float* ok, int* oi,
+__device__ bool block_bucket_topk(float* key, int* idx, int n, int k, float* ok, int* oi,
                                   unsigned* cnt, int nb, unsigned* red) {
     const int t = threadIdx.x;
     for (int b = t; b < nb; b += NT) cnt[b] = 0u;
@@ -344,20 +346,49 @@ __device__ bool block_bucket_topk(const float* key, const int* idx, int n, int k
     auto bin_of = [&](float v) { return min(nb - 1, static_cast<int>((v - lo) * scale)); };
     for (int e = t; e < n; e += NT) atomicAdd(cnt + bin_of(key[e]), 1u);
     __syncthreads();
-    // counts -> starts; thread t owns bins [t per, t per + per)
+    // counts -> starts; thread t owns bins [t per, t per + per), read and
+    // written as 16-byte vectors when per >= 4 (cnt 16-byte aligned): scalar
+    // accesses at stride per would conflict per-way on the banks
     const int per = (nb + NT - 1) / NT;
     const int b0 = min(nb, t * per), b1 = min(nb, b0 + per);
-    int own = 0;
-    for (int b = b0; b < b1; ++b) own += static_cast<int>(cnt[b]);
-    int total = 0;
-    int run = block_exclusive_scan<NT>(own, &total);
     unsigned flag = 0u;
-    for (int b = b0; b < b1; ++b) {
-        const int c = static_cast<int>(cnt[b]);
-        if (run < k && c > 32) flag = 1u;
-        if (run < k && k <= run + c) flag |= static_cast<unsigned>(b) << 1;
-        cnt[b] = static_cast<unsigned>(run);
-        run += c;
+    int total = 0;
+    if (per == 4 || per == 8) {  // nb = per NT: b1 - b0 == per
+        uint4 c4[2];
+        int own = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (4 * h < per) {
+                c4[h] = *reinterpret_cast<const uint4*>(cnt + b0 + 4 * h);
+                own += static_cast<int>(c4[h].x + c4[h].y + c4[h].z + c4[h].w);
+            }
+        int run = block_exclusive_scan<NT>(own, &total);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (4 * h < per) {
+                unsigned c[4] = {c4[h].x, c4[h].y, c4[h].z, c4[h].w};
+                unsigned st[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int cj = static_cast<int>(c[j]);
+                    if (run < k && cj > 32) flag = 1u;
+                    if (run < k && k <= run + cj) flag |= static_cast<unsigned>(b0 + 4 * h + j) << 1;
+                    st[j] = static_cast<unsigned>(run);
+                    run += cj;
+                }
+                *reinterpret_cast<uint4*>(cnt + b0 + 4 * h) = make_uint4(st[0], st[1], st[2], st[3]);
+            }
+    } else {
+        int own = 0;
+        for (int b = b0; b < b1; ++b) own += static_cast<int>(cnt[b]);
+        int run = block_exclusive_scan<NT>(own, &total);
+        for (int b = b0; b < b1; ++b) {
+            const int c = static_cast<int>(cnt[b]);
+            if (run < k && c > 32) flag = 1u;
+            if (run < k && k <= run + c) flag |= static_cast<unsigned>(b) << 1;
+            cnt[b] = static_cast<unsigned>(run);
+            run += c;
+        }
     }
     if (flag) atomicOr(red + 2, flag);
     __syncthreads();
@@ -373,21 +404,19 @@ __device__ bool block_bucket_topk(const float* key, const int* idx, int n, int k
             oi[pos] = idx[e];
         }
     }
-    __syncthreads();  // cnt[b] = end of bin b
-    for (int b = t; b <= bk; b += NT) {
+    __syncthreads();  // cnt[b] = end of bin b; key / idx are free
+    // final places: an entry's rank inside its bin (<= 32 entries) under the
+    // (key, index) order, one thread per entry
+    const int nout = static_cast<int>(cnt[bk]);
+    for (int x = t; x < nout; x += NT) {
+        const float kx = ok[x];
+        const int ix = oi[x];
+        const int b = bin_of(kx);
         const int s0 = b > 0 ? static_cast<int>(cnt[b - 1]) : 0, s1 = static_cast<int>(cnt[b]);
-        for (int x = s0 + 1; x < s1; ++x) {
-            const float kx = ok[x];
-            const int ix = oi[x];
-            int u = x;
-            while (u > s0 && pair_less(kx, ix, ok[u - 1], oi[u - 1])) {
-                ok[u] = ok[u - 1];
-                oi[u] = oi[u - 1];
-                --u;
-            }
-            ok[u] = kx;
-            oi[u] = ix;
-        }
+        int r = s0;
+        for (int y = s0; y < s1; ++y) r += pair_less(ok[y], oi[y], kx, ix) ? 1 : 0;
+        key[r] = kx;
+        idx[r] = ix;
     }
     __syncthreads();
     return true;

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
     int* si = reinterpret_cast<int*>(sk + NCC);         // [NCC] candidate indices
     float* ok = reinterpret_cast<float*>(si + NCC);     // [k + 32] bucket output keys
     int* oi = reinterpret_cast<int*>(ok + k + 32);      // [k + 32] bucket output indices
-    unsigned* cnt = reinterpret_cast<unsigned*>(oi + k + 32);  // [NCC] bucket counters
+    unsigned* cnt = reinterpret_cast<unsigned*>(                 // [NCC] bucket counters, 16 B aligned
+        (reinterpret_cast<uintptr_t>(oi + k + 32) + 15) & ~static_cast<uintptr_t>(15));
     __shared__ int s_np[32];
     __shared__ int s_total, s_nc, s_bin;
     __shared__ unsigned s_red[3];
@@ -77,6 +78,23 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
     const int total = s_total;
     const float T0 = a.f.t0[q];
     auto logp = [&](int p) { return a.f.vlog + ((p0 + p) * TILE + row) * a.f.CV; };
+    // every logged value of the query (part by part), LU loads in flight per
+    // thread before any is used: the passes are latency-bound otherwise
+    // (one L2 round trip per NT values)
+    constexpr int LU = 8;
+    auto for_each_value = [&](auto&& fn) {
+        for (int p = 0; p < nparts; ++p) {
+            const float2* src = logp(p);
+            const int np = s_np[p];
+            for (int e0 = t; e0 < np; e0 += LU * NT) {
+                float v[LU];
+#pragma unroll
+                for (int u = 0; u < LU; ++u) v[u] = e0 + u * NT < np ? __ldg(&src[e0 + u * NT].x) : kInf;
+#pragma unroll
+                for (int u = 0; u < LU; ++u) fn(v[u]);
+            }
+        }
+    };
     bool ok_q = total >= k;
     float tau = kInf;
     int nc = 0;
@@ -84,17 +102,12 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
         // 1. the bound: extremes of the finite values (a log holds +inf padding
         //    references when its threshold is infinite; they never count)
         unsigned lo_l = 0xffffffffu, hi_l = 0u;
-        for (int p = 0; p < nparts; ++p) {
-            const float2* src = logp(p);
-            const int np = s_np[p];
-            for (int e = t; e < np; e += NT) {
-                const float v = __ldg(&src[e].x);
-                if (v < kInf) {
-                    lo_l = min(lo_l, ord(v));
-                    hi_l = max(hi_l, ord(v));
-                }
+        for_each_value([&](float v) {
+            if (v < kInf) {
+                lo_l = min(lo_l, ord(v));
+                hi_l = max(hi_l, ord(v));
             }
-        }
+        });
         lo_l = __reduce_min_sync(0xffffffffu, lo_l);
         hi_l = __reduce_max_sync(0xffffffffu, hi_l);
         if (lane == 0) {
@@ -106,14 +119,9 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
         const float hi_f = fminf(T0, unord(s_red[1]));
         const float scale = hi_f > lo ? 256.f / (hi_f - lo) : 0.f;
         auto bin_of = [&](float v) { return min(255, max(0, static_cast<int>((v - lo) * scale))); };
-        for (int p = 0; p < nparts; ++p) {
-            const float2* src = logp(p);
-            const int np = s_np[p];
-            for (int e = t; e < np; e += NT) {
-                const float v = __ldg(&src[e].x);
-                if (v < kInf) atomicAdd(s_hist + bin_of(v), 1u);
-            }
-        }
+        for_each_value([&](float v) {
+            if (v < kInf) atomicAdd(s_hist + bin_of(v), 1u);
+        });
         __syncthreads();
         if (t < 32) {  // warp 0: the bin where the running count reaches k
             unsigned c[8], tot = 0;
@@ -144,14 +152,9 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
         const int bk = s_bin;
         unsigned mx = 0u;
         if (bk >= 0)
-            for (int p = 0; p < nparts; ++p) {
-                const float2* src = logp(p);
-                const int np = s_np[p];
-                for (int e = t; e < np; e += NT) {
-                    const float v = __ldg(&src[e].x);
-                    if (v < kInf && bin_of(v) <= bk) mx = max(mx, ord(v));
-                }
-            }
+            for_each_value([&](float v) {
+                if (v < kInf && bin_of(v) <= bk) mx = max(mx, ord(v));
+            });
         mx = __reduce_max_sync(0xffffffffu, mx);
         if (lane == 0) atomicMax(s_red + 2, mx);
         __syncthreads();
@@ -164,17 +167,24 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
             for (int p = 0; p < nparts; ++p) {
                 const float2* src = logp(p);
                 const int np = s_np[p];
-                for (int e0 = 0; e0 < np; e0 += NT) {
-                    const int e = e0 + t;
-                    float2 r = make_float2(kInf, 0.f);
-                    if (e < np) r = __ldg(&src[e]);
-                    const bool in = r.x <= tau;
-                    const unsigned bal = __ballot_sync(0xffffffffu, in);
-                    int base = 0;
-                    if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    const int pos = base + __popc(bal & ((1u << lane) - 1u));
-                    if (in && pos < NCC) si[pos] = __float_as_int(r.y);
+                constexpr int CU = 4;
+                for (int e0 = 0; e0 < np; e0 += CU * NT) {
+                    float2 r[CU];
+#pragma unroll
+                    for (int u = 0; u < CU; ++u) {
+                        const int e = e0 + u * NT + t;
+                        r[u] = e < np ? __ldg(&src[e]) : make_float2(kInf, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < CU; ++u) {
+                        const bool in = r[u].x <= tau;
+                        const unsigned bal = __ballot_sync(0xffffffffu, in);
+                        int base = 0;
+                        if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        const int pos = base + __popc(bal & ((1u << lane) - 1u));
+                        if (in && pos < NCC) si[pos] = __float_as_int(r[u].y);
+                    }
                 }
             }
             __syncthreads();
@@ -199,16 +209,14 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
     // 5. the k smallest: bucket sort, or (dense ties) a bitonic sort of all
     int nbk = 32;
     while (nbk < nc) nbk <<= 1;
-    float* rk = ok;
-    int* ri = oi;
+    float* rk = sk;
+    int* ri = si;
     if (!block_bucket_topk<NT>(sk, si, nc, k, ok, oi, cnt, nbk, s_red)) {
         for (int e = nc + t; e < nbk; e += NT) {
             sk[e] = kInf;
             si[e] = 0x7fffffff;
         }
         bitonic_sort_kv(sk, si, nbk);
-        rk = sk;
-        ri = si;
     }
     // finalize: sqrt, then equal reported distances in ascending index order
     if (!a.raw_keys) {
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
 
 void launch_select_large(const LargeArgs& la, cudaStream_t stream) {
     // candidates [NC] keys + indices, bucket output [k + 32] x 2, counters [NC]
-    const size_t smem = static_cast<size_t>(la.NC) * 12 + static_cast<size_t>(la.k + 32) * 8;
+    const size_t smem = static_cast<size_t>(la.NC) * 12 + static_cast<size_t>(la.k + 32) * 8 + 16;
     const int nt = la.NC <= 512 ? 64 : la.NC <= 1024 ? 128 : 256;
     auto sel = nt == 64 ? select_large_kernel<64> : nt == 128 ? select_large_kernel<128> : select_large_kernel<256>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize,
