@@ -12,6 +12,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -57,13 +59,37 @@ void check_point_set(const float* data, int64_t n, int64_t d, bool check_values)
 // Device-side PointSet value check (point_set.hpp:27-31): first index of a
 // non-finite coordinate (atomicMin), so the host API validates a device copy
 // in microseconds instead of scanning n*d values on one host core.
+unsigned scan_grid(int64_t count);
+
+// 16-byte loads over the aligned middle, four in flight per thread.
 __global__ void finite_scan_kernel(const float* X, int64_t count, unsigned long long* first,
                                    int64_t base = 0) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-         i += stride) {
-        if (!isfinite(__ldg(X + i))) atomicMin(first, static_cast<unsigned long long>(base + i));
+    const int64_t h = std::min<int64_t>(count, ((16 - (reinterpret_cast<uintptr_t>(X) & 15)) & 15) / 4);
+    const int64_t n4 = (count - h) / 4;
+    const float4* X4 = reinterpret_cast<const float4*>(X + h);
+    auto bad = [&](int64_t i) { atomicMin(first, static_cast<unsigned long long>(base + i)); };
+    for (int64_t i = t; i < h; i += stride)
+        if (!isfinite(__ldg(X + i))) bad(i);
+    for (int64_t i0 = t; i0 < n4; i0 += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            v[u] = i0 + u * stride < n4 ? __ldg(X4 + i0 + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float c[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (!isfinite(c[j])) {
+                    bad(h + 4 * (i0 + u * stride) + j);
+                    break;
+                }
+        }
     }
+    for (int64_t i = h + 4 * n4 + t; i < count; i += stride)
+        if (!isfinite(__ldg(X + i))) bad(i);
 }
 
 // No CUDA device (e.g. a CPU-only CI box): validate on the host so argument
@@ -88,17 +114,31 @@ void throw_non_finite(unsigned long long i, int64_t d) {
 // APIs: first non-finite coordinate, with the reference's message.
 void check_finite_device(cudaStream_t s, const float* X, int64_t rows, int64_t d,
                          unsigned long long* dbad) {
+    // persistent per-device result slot (device) and pinned host copy: no
+    // allocation per call (a stream-ordered malloc/free pair re-maps pool
+    // memory after every synchronisation -- hundreds of microseconds)
+    struct Slots {
+        unsigned long long* dev = nullptr;
+        unsigned long long* host = nullptr;
+    };
+    static std::mutex mu;
+    static std::map<int, Slots> per_device;
+    int device = 0;
+    KNN_CUDA_CHECK(cudaGetDevice(&device));
+    std::lock_guard<std::mutex> lock(mu);  // one check at a time per process (slot reuse)
+    Slots& sl = per_device[device];
+    if (!sl.dev) {
+        KNN_CUDA_CHECK(cudaMalloc(&sl.dev, sizeof(unsigned long long)));
+        KNN_CUDA_CHECK(cudaMallocHost(&sl.host, sizeof(unsigned long long)));
+    }
+    unsigned long long* tmp = dbad ? dbad : sl.dev;
     const int64_t count = rows * d;
-    unsigned long long* tmp = dbad;
-    if (!tmp) KNN_CUDA_CHECK(cudaMallocAsync(&tmp, sizeof(unsigned long long), s));
     KNN_CUDA_CHECK(cudaMemsetAsync(tmp, 0xff, sizeof(unsigned long long), s));
-    finite_scan_kernel<<<static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 1184)), 256, 0, s>>>(
-        X, count, tmp);
+    finite_scan_kernel<<<scan_grid(count), 256, 0, s>>>(X, count, tmp);
     KNN_LAUNCH_CHECK();
-    unsigned long long bad = 0;
-    KNN_CUDA_CHECK(cudaMemcpyAsync(&bad, tmp, sizeof(bad), cudaMemcpyDeviceToHost, s));
-    if (!dbad) KNN_CUDA_CHECK(cudaFreeAsync(tmp, s));
+    KNN_CUDA_CHECK(cudaMemcpyAsync(sl.host, tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     KNN_CUDA_CHECK(cudaStreamSynchronize(s));
+    const unsigned long long bad = *sl.host;
     if (bad != ~0ull) throw_non_finite(bad, d);
 }
 

@@ -78,6 +78,14 @@ DeviceContext& context_for(int device) {
         slot = std::make_unique<DeviceContext>();
         slot->device = device;
         KNN_CUDA_CHECK(cudaSetDevice(device));
+        // stream-ordered allocations (cudaMallocAsync) stay cached in the
+        // device's default pool across synchronisations instead of being
+        // unmapped at every one (release threshold 0) and re-mapped next call
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            KNN_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
         KNN_CUDA_CHECK(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
         KNN_CUDA_CHECK(cudaStreamCreateWithFlags(&slot->copy_stream, cudaStreamNonBlocking));
         for (auto& e : slot->ev) KNN_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
