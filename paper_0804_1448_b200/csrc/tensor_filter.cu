@@ -16,6 +16,10 @@ namespace tp {
 
 namespace {
 
+#ifndef KNN_DRAIN_BATCH
+#define KNN_DRAIN_BATCH 1  // 0: drains insert one buffered minimum per round (dev A/B)
+#endif
+
 // Dev-only filter modes (KNN_B200_FILTER_MODE: 2 no epilogue work, 3 no pushes,
 // used to measure floors); compiled out of the product build, where the hot
 // loop carries no mode checks.
@@ -127,7 +131,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     do {                                                                                         \
         const int nb = static_cast<int>((sgp - sg0) / (EPI_THREADS * 4));                       \
         const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
-        _Pragma("unroll 1") for (int j_ = 0; j_ < mx_; ++j_) {                                   \
+        int j_ = 0;                                                                              \
+        /* five or more rounds left: batches of 8 through the merge network */                 \
+        if constexpr (KNN_DRAIN_BATCH && KR <= 24)                                               \
+            _Pragma("unroll 1") for (; j_ + 4 < mx_; j_ += 8) {                                  \
+                float b_[8];                                                                     \
+                int nv_ = 0;                                                                     \
+                _Pragma("unroll") for (int u_ = 0; u_ < 8; ++u_) {                               \
+                    float g_ = j_ + u_ < nb ? lds_f32(sg0 + (j_ + u_) * (EPI_THREADS * 4)) : kInf; \
+                    g_ = g_ <= Tf && g_ < L.key[KR - 1] ? g_ : kInf;                             \
+                    b_[u_] = g_;                                                                 \
+                    nv_ += g_ < kInf ? 1 : 0;                                                    \
+                }                                                                                \
+                if (__any_sync(0xffffffffu, nv_ > 0)) L.insert8(b_, nv_);                        \
+            }                                                                                    \
+        _Pragma("unroll 1") for (; j_ < mx_; ++j_) {                                             \
             const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
             /* a minimum at or above the list's last entry changes nothing */                  \
             if (__any_sync(0xffffffffu, g_ <= Tf && g_ < L.key[KR - 1])) L.insert(g_);           \
