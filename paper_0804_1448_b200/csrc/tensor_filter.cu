@@ -16,6 +16,9 @@ namespace tp {
 
 namespace {
 
+#ifndef KNN_BATCH_MIN
+#define KNN_BATCH_MIN 5  // rounds left for a batch (fewer: one rank insert per round)
+#endif
 #ifndef KNN_DRAIN_BATCH
 #define KNN_DRAIN_BATCH 1  // 0: drains insert one buffered minimum per round (dev A/B)
 #endif
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int j_ = 0;                                                                              \
         /* five or more rounds left: batches of 8 through the merge network */                 \
         if constexpr (KNN_DRAIN_BATCH && KR <= 24)                                               \
-            _Pragma("unroll 1") for (; j_ + 4 < mx_; j_ += 8) {                                  \
+            _Pragma("unroll 1") for (; j_ + KNN_BATCH_MIN - 1 < mx_; j_ += 8) {                  \
                 float b_[8];                                                                     \
                 int nv_ = 0;                                                                     \
                 _Pragma("unroll") for (int u_ = 0; u_ < 8; ++u_) {                               \

@@ -163,7 +163,10 @@ constexpr bool kStats = true;
 constexpr bool kStats = false;
 #endif
 
-constexpr int CAP = 24;        // per-lane buffered group minima awaiting the bound list (smem);
+#ifndef KNN_CAP
+#define KNN_CAP 24
+#endif
+constexpr int CAP = KNN_CAP;   // per-lane buffered group minima awaiting the bound list (smem);
                                // drained once per tile (a tile pushes <= 16), off the TMEM path
 constexpr int EPI_REGS = 232;  // setmaxnreg: epilogue warpgroups grow by what warpgroup 0 frees
 // (the pool is the CTA's launch allocation: 2 x 128 x (232 - 168) = 128 x (168 - 40))
