@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
     sm100::pdl_wait();  // device fallback: the re-rank's query list is complete
     const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
     if (n_eff <= 0) return;
-    const ExactSplit sp = exact_split(n_eff, a.ntiles, gridDim.x);
+    const ExactSplit sp = exact_split(n_eff, a.ntiles, gridDim.x, a.min_tiles);
     if (blockIdx.x >= sp.G) return;
     int64_t u = sp.start(blockIdx.x);
     const int64_t u_end = sp.start(blockIdx.x + 1);
@@ -155,6 +155,13 @@ __global__ void __launch_bounds__(THREADS, 2) exact_knn_kernel(ExactArgs a) {
                     WarpList<int32_t> L{Lk + row * a.k, Li + row * a.k, a.k};
                     L.init(lane);
                 }
+            __syncwarp();
+            // rows past the query count (a partial last block; the few-query
+            // device fallback) get a -inf threshold: never offered a key
+            if (lane < 16) {
+                const int row = 2 * warp + (lane & 1) + 16 * (lane >> 1);
+                if (q0 + row >= n_eff) Lk[row * a.k + a.k - 1] = -kInf;
+            }
         }
         __syncwarp();
 
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(MX_WARPS * 32) merge_exact_kernel(ExactArgs a,
     const int k = a.k;
     sm100::pdl_wait();  // the exact kernel's segment slots are complete
     const int64_t n_eff = a.qcount ? min(a.n, static_cast<int64_t>(*a.qcount)) : a.n;
-    const ExactSplit sp = exact_split(n_eff, a.ntiles, a.max_ctas);
+    const ExactSplit sp = exact_split(n_eff, a.ntiles, a.max_ctas, a.min_tiles);
     for (int64_t q = static_cast<int64_t>(blockIdx.x) * MX_WARPS + warp; q < n_eff;
          q += static_cast<int64_t>(gridDim.x) * MX_WARPS) {
         const int64_t b = q / QT;
@@ -446,6 +453,10 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
     const bool smem_lists = a.glist_key == nullptr;
     const size_t smem = smem_bytes(a.k, smem_lists);
     a.max_ctas = exact_max_ctas(a.k, smem_lists);
+    // 8 tiles per CTA at least (spreading a few-query block over fewer CTAs,
+    // max(8, k / 4) tiles, measured slower for one fallback query at k = 100:
+    // the merge saves 0.11 ms, the longer CTA chains cost 0.27 ms)
+    a.min_tiles = 8;
     const int kp = (a.k + 31) / 32;
     // INDIRECT (query list, device-side count): the certification fallback of
     // the tensor path, small and large k
@@ -465,7 +476,7 @@ void launch_exact_m(const ExactArgs& a_in, cudaStream_t stream) {
     KNN_LAUNCH_CHECK();
     // merge the blocks spread over several CTAs (host-known counts: only if any)
     if (!a.qcount) {
-        const ExactSplit sp = exact_split(a.n, a.ntiles, a.max_ctas);
+        const ExactSplit sp = exact_split(a.n, a.ntiles, a.max_ctas, a.min_tiles);
         const int64_t nqb = (a.n + QT - 1) / QT;
         bool any = false;
         for (int64_t b = 0; b < nqb && !any; ++b)
@@ -500,6 +511,7 @@ void launch_exact_log_m(const ExactArgs& a_in, cudaStream_t stream) {
     ExactArgs a = a_in;
     const size_t smem = smem_bytes(a.k, false) + 2 * QT * sizeof(float);
     a.max_ctas = exact_log_max_ctas();
+    a.min_tiles = 0;  // the default split (exact_large's select re-derives it)
     auto kern = a.qlist ? exact_knn_kernel<M, kLogKP, true> : exact_knn_kernel<M, kLogKP>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));

@@ -28,6 +28,7 @@ struct ExactArgs {
     float* mglist_key;       // merge list scratch (n x k) when k > 2048
     int64_t* mglist_idx;
     int max_ctas;            // set by launch_exact (grid of the exact kernel)
+    int min_tiles;           // set by launch_exact: reference tiles per CTA at least (0: 8)
     // threshold-log mode (large k, exact_large.cu): instead of lists, every key
     // <= t0[q * t0_stride] is appended as {key, index bits} to the segment's
     // log vlog[slot][128][CV] (column order), its length to vlog_n[slot][128]
@@ -47,11 +48,12 @@ struct ExactSplit {
     __host__ __device__ int64_t start(int64_t c) const { return c * units / G; }
     __host__ __device__ int64_t cta_of(int64_t x) const { return ((x + 1) * G + units - 1) / units - 1; }
 };
-__host__ __device__ inline ExactSplit exact_split(int64_t n, int ntiles, int max_ctas) {
+__host__ __device__ inline ExactSplit exact_split(int64_t n, int ntiles, int max_ctas, int min_tiles = 8) {
     const int64_t nqb = (n + 127) / 128;
     ExactSplit s;
     s.units = nqb * ntiles;
-    const int64_t by_work = s.units / 8 > 1 ? s.units / 8 : 1;
+    const int64_t per = min_tiles > 8 ? min_tiles : 8;
+    const int64_t by_work = s.units / per > 1 ? s.units / per : 1;
     s.G = by_work < max_ctas ? by_work : max_ctas;
     return s;
 }
