@@ -303,7 +303,9 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         // histogram bin above A_(k)); more -> the query takes the exact path
         int NC = 64;
         while (NC < k + k / 2 + 64) NC <<= 1;
-        la.NC = NC;
+        if (const char* e = std::getenv("KNN_B200_SELECT_NC_MULT"))  // dev
+            NC *= std::max(1, std::atoi(e));
+        la.NC = std::min(NC, 8192);
         la.f = fa;
         la.raw_keys = raw_keys;
         la.index_base = index_base;

@@ -24,9 +24,9 @@ using namespace sel;
 // Large-k selection, one block per query.  The query's value logs (one per
 // part slot, {A, index}) stay in global memory and are streamed (L1/L2 hits
 // after the first pass); shared memory holds only the candidates:
-//  1. a bound B >= A_(k): min / max, then a 256-bin histogram over
-//     [min, min(max, T0)], then the largest value in the bins up to the one
-//     where the running count reaches k (at most one bin above A_(k));
+//  1. a bound B >= A_(k): a 256-bin histogram over [-|q~|^2, T0], B = the upper
+//     edge of the bin where the running count reaches k (at most one bin
+//     above A_(k));
 //  2. certificate: >= k values logged, no log overflowed, thresh(B) <= T0
 //     (every reference with A <= tau = thresh(B) was logged);
 //  3. candidates = logged values <= tau (warp-aggregated appends, at most NCC);
@@ -99,25 +99,25 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
     float tau = kInf;
     int nc = 0;
     if (ok_q) {
-        // 1. the bound: extremes of the finite values (a log holds +inf padding
-        //    references when its threshold is infinite; they never count)
-        unsigned lo_l = 0xffffffffu, hi_l = 0u;
-        for_each_value([&](float v) {
-            if (v < kInf) {
-                lo_l = min(lo_l, ord(v));
-                hi_l = max(hi_l, ord(v));
-            }
-        });
-        lo_l = __reduce_min_sync(0xffffffffu, lo_l);
-        hi_l = __reduce_max_sync(0xffffffffu, hi_l);
-        if (lane == 0) {
-            atomicMin(s_red, lo_l);
-            atomicMax(s_red + 1, hi_l);
+        // 1. the bound.  256 bins over [lo, T0]: every logged value is <= T0,
+        //    and A = D^2 - ||q~||^2 >= lo = -(||q~||^2 + eps) up to rounding
+        //    (below lo -> bin 0).  Only when T0 is infinite (everything was
+        //    logged, +inf padding included) a first pass finds the largest
+        //    finite value.
+        const Consts qc = load_consts(a.f, q);
+        const float lo = -(qc.nq + qc.eps);
+        float hi_f = T0;
+        if (!(T0 < kInf)) {  // block-uniform
+            unsigned hi_l = 0u;
+            for_each_value([&](float v) {
+                if (v < kInf) hi_l = max(hi_l, ord(v));
+            });
+            hi_l = __reduce_max_sync(0xffffffffu, hi_l);
+            if (lane == 0) atomicMax(s_red + 1, hi_l);
+            __syncthreads();
+            hi_f = unord(s_red[1]);
         }
-        __syncthreads();
-        const float lo = unord(s_red[0]);
-        const float hi_f = fminf(T0, unord(s_red[1]));
-        const float scale = hi_f > lo ? 256.f / (hi_f - lo) : 0.f;
+        const float scale = hi_f > lo && hi_f < kInf ? 256.f / (hi_f - lo) : 0.f;
         auto bin_of = [&](float v) { return min(255, max(0, static_cast<int>((v - lo) * scale))); };
         for_each_value([&](float v) {
             if (v < kInf) atomicAdd(s_hist + bin_of(v), 1u);
@@ -150,17 +150,18 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
         }
         __syncthreads();
         const int bk = s_bin;
-        unsigned mx = 0u;
+        // B = the upper edge of bin bk: >= every value in the bins up to bk,
+        // so >= A_(k) (the margin, 2^-18 of the larger magnitude, covers the
+        // roundings of (v - lo) * scale and of the edge); the last bin's edge
+        // is hi_f itself
+        float B = kInf;
         if (bk >= 0)
-            for_each_value([&](float v) {
-                if (v < kInf && bin_of(v) <= bk) mx = max(mx, ord(v));
-            });
-        mx = __reduce_max_sync(0xffffffffu, mx);
-        if (lane == 0) atomicMax(s_red + 2, mx);
-        __syncthreads();
+            B = bk == 255 || !(scale > 0.f)
+                    ? hi_f
+                    : fminf(hi_f, lo + static_cast<float>(bk + 1) / scale +
+                                      (fabsf(lo) + fabsf(hi_f)) * 0x1.0p-18f);
         // 2. certificate
-        const Consts qc = load_consts(a.f, q);
-        tau = bk >= 0 ? thresh(unord(s_red[2]), qc) : kInf;
+        tau = bk >= 0 ? thresh(B, qc) : kInf;
         ok_q = tau <= T0;  // every reference with A <= tau was logged
         if (ok_q) {
             // 3. candidates: warp-aggregated appends (order is irrelevant)
@@ -252,8 +253,12 @@ __global__ void __launch_bounds__(NT, 65536 / (NT * 64)) select_large_kernel(Lar
 void launch_select_large(const LargeArgs& la, cudaStream_t stream) {
     // candidates [NC] keys + indices, bucket output [k + 32] x 2, counters [NC]
     const size_t smem = static_cast<size_t>(la.NC) * 12 + static_cast<size_t>(la.k + 32) * 8 + 16;
-    const int nt = la.NC <= 512 ? 64 : la.NC <= 1024 ? 128 : 256;
-    auto sel = nt == 64 ? select_large_kernel<64> : nt == 128 ? select_large_kernel<128> : select_large_kernel<256>;
+    // the fewest threads with <= 8 candidates each (<= 16 for the bitonic
+    // fallback's register network)
+    const int nt = la.NC <= 512 ? 64 : la.NC <= 1024 ? 128 : la.NC <= 2048 ? 256 : 512;
+    auto sel = nt == 64    ? select_large_kernel<64>
+               : nt == 128 ? select_large_kernel<128>
+               : nt == 256 ? select_large_kernel<256> : select_large_kernel<512>;
     KNN_CUDA_CHECK(cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     {

@@ -352,9 +352,9 @@ def test_device_fallback_is_asynchronous_on_a_stream(knn, oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", [33, 64, 129, 500])
+@pytest.mark.parametrize("k", [33, 64, 129, 500, 1000])
 def test_large_k_block_sizes(knn, oracle, k):
-    """The large-k selection picks 64 / 128 / 256 / 512-thread blocks from the
+    """The large-k selection picks 64 / 128 / 256-thread blocks from the
     candidate capacity; every size must give the exact table."""
     m, d = 12000, 24
     R = oracle.uniform_f32(m, d, 600 + k)
@@ -365,6 +365,26 @@ def test_large_k_block_sizes(knn, oracle, k):
     assert rep.ok, f"k={k}: {rep}"
     te = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
     assert (t.index == te.index).all() and (t.distance == te.distance).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [8, 16, 32, 64, 128])
+@pytest.mark.parametrize("k", [100, 256])
+def test_large_k_certifies_uniform_data(knn, oracle, d, k):
+    """On uniform data every query certifies at every d: the select's bound
+    bins must cover negative A (= D^2 - |q~|^2, the low-d case) and its
+    candidate capacity must hold the values inside thresh(B) -- a failure here
+    is silent in the results (the exact fallback answers) but costs the exact
+    path's time."""
+    m, n = 20000, 256
+    R = oracle.uniform_f32(m, d, 810 + d + k)
+    Q = oracle.uniform_f32(n, d, 820 + d + k)
+    t = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() == 0, f"d={d} k={k}: {knn.last_fallback_count()} fallbacks"
+    rows = np.arange(0, n, 8)
+    ri, rd = oracle.knn(Q[rows], R, k)
+    rep = compare(t.index[rows], t.distance[rows], ri, rd, Q[rows], R, oracle=oracle)
+    assert rep.ok, f"d={d} k={k}: {rep}"
 
 
 @pytest.mark.gpu
