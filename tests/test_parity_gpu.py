@@ -368,6 +368,23 @@ def test_large_k_block_sizes(knn, oracle, k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("k", [100, 300])
+def test_large_k_duplicate_ties(knn, oracle, k):
+    """Large k on duplicate-heavy references (40 copies of each point): runs of
+    40 equal exact keys overfill the select's buckets (<= 32 entries), so the
+    bitonic sort of all candidates takes over; ties resolve by ascending index,
+    bitwise the exact path's table."""
+    base = oracle.uniform_f32(150, 16, 36)
+    Rd = np.repeat(base, 40, axis=0)
+    Qd = oracle.uniform_f32(64, 16, 37)
+    td = knn.bf_knn(Qd, Rd, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    te = knn.bf_knn(Qd, Rd, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (td.index == te.index).all() and (td.distance == te.distance).all()
+    ri, rd = oracle.knn(Qd, Rd, k)
+    assert compare(td.index, td.distance, ri, rd, Qd, Rd, oracle=oracle).ok
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("d", [8, 16, 32, 64, 128])
 @pytest.mark.parametrize("k", [100, 256])
 def test_large_k_certifies_uniform_data(knn, oracle, d, k):
