@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int mx_ = __reduce_max_sync(0xffffffffu, nb);                                      \
         int j_ = 0;                                                                              \
         /* five or more rounds left: batches of 8 through the merge network */                 \
-        if constexpr (KNN_DRAIN_BATCH && KR <= 24)                                               \
+        if constexpr (KNN_DRAIN_BATCH && KR <= 24) {                                             \
             _Pragma("unroll 1") for (; j_ + KNN_BATCH_MIN - 1 < mx_; j_ += 8) {                  \
                 float b_[8];                                                                     \
                 int nv_ = 0;                                                                     \
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }                                                                                \
                 if (__any_sync(0xffffffffu, nv_ > 0)) L.insert8(b_, nv_);                        \
             }                                                                                    \
+        }                                                                                        \
         _Pragma("unroll 1") for (; j_ < mx_; ++j_) {                                             \
             const float g_ = j_ < nb ? lds_f32(sg0 + j_ * (EPI_THREADS * 4)) : kInf;             \
             /* a minimum at or above the list's last entry changes nothing */                  \

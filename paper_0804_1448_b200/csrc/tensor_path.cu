@@ -127,8 +127,14 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
     if (large)
         if (const char* e = std::getenv("KNN_B200_LARGE_MARGIN")) margin = std::max(1, std::atoi(e));  // dev
     // at most ~29 CTAs share a query-tile pair, so a query has <= 32 partial lists
+    // CTAs per query-tile pair: at least ~6 units each (every CTA part of a
+    // pair restarts its bound list, so short parts push most of their groups
+    // and the re-rank merges more lists; config A, 4800^2: 6 per pair instead
+    // of 8, filter + re-rank 70 -> 66 us); at most 29 (<= 32 list slots)
+    int per_pair = std::max(1, std::min(29, rtiles / 6));
+    if (const char* e = std::getenv("KNN_B200_CTAS_PER_PAIR")) per_pair = std::max(1, std::min(29, std::atoi(e)));  // dev
     const int G = static_cast<int>(std::min<int64_t>(std::min<int64_t>(kSmCount, U),
-                                                     static_cast<int64_t>(pairs) * 29));
+                                                     static_cast<int64_t>(pairs) * per_pair));
     // partial-list slots per query tile under the stream-K split
     int S_max = 1;
     for (int pp = 0; pp < pairs; ++pp) {

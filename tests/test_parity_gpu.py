@@ -368,6 +368,24 @@ def test_large_k_block_sizes(knn, oracle, k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("k", [21, 28, 32])
+def test_small_k_32_entry_lists(knn, oracle, k):
+    """k = 21 .. 32 runs the filter with 32-entry bound lists (no batched
+    drains), with several units per CTA: exact table, every query certified."""
+    m, n, d = 20000, 2048, 29
+    R = oracle.uniform_f32(m, d, 840 + k)
+    Q = oracle.uniform_f32(n, d, 850 + k)
+    t = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+    assert knn.last_fallback_count() == 0
+    rows = np.arange(0, n, 16)
+    ri, rd = oracle.knn(Q[rows], R, k)
+    rep = compare(t.index[rows], t.distance[rows], ri, rd, Q[rows], R, oracle=oracle)
+    assert rep.ok, f"k={k}: {rep}"
+    te = knn.bf_knn(Q[rows], R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (t.index[rows] == te.index).all() and (t.distance[rows] == te.distance).all()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("k", [100, 300])
 def test_large_k_duplicate_ties(knn, oracle, k):
     """Large k on duplicate-heavy references (40 copies of each point): runs of

@@ -24,6 +24,7 @@ run(50, 9000, 16, 20, path=knn.PATH_TENSOR, R=dup)
 # threshold-log selection over a query list), the exact path's large-k
 # selection (L1 / L2 with d > 128) and its forced list-path fallback
 run(300, 5000, 128, 20, path=knn.PATH_TENSOR)
+run(600, 20000, 29, 28, path=knn.PATH_TENSOR)  # 32-entry bound lists, several units per CTA
 run(300, 5000, 64, 150, path=knn.PATH_TENSOR)
 run(50, 9000, 16, 64, path=knn.PATH_TENSOR, R=dup)
 run(50, 9000, 16, 300, path=knn.PATH_TENSOR, R=dup)
