@@ -368,6 +368,22 @@ def test_large_k_block_sizes(knn, oracle, k):
 
 
 @pytest.mark.gpu
+def test_every_k_tensor_equals_exact(knn, oracle):
+    """Every k from 1 to 40 (each bound-list size, the small/large switch)
+    and large k up to 1024 on one shape: the tensor path's table is bitwise
+    the exact path's on a query sample, with every query certified."""
+    m, n, d = 20000, 2048, 29
+    R = oracle.uniform_f32(m, d, 861)
+    Q = oracle.uniform_f32(n, d, 862)
+    rows = np.arange(0, n, 32)
+    for k in list(range(1, 41)) + [64, 100, 129, 256, 500, 1024]:
+        t = knn.bf_knn(Q, R, k, config=knn.BfConfig(path=knn.PATH_TENSOR))
+        assert knn.last_fallback_count() == 0, f"k={k}"
+        te = knn.bf_knn(Q[rows], R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+        assert (t.index[rows] == te.index).all() and (t.distance[rows] == te.distance).all(), f"k={k}"
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("k", [21, 28, 32])
 def test_small_k_32_entry_lists(knn, oracle, k):
     """k = 21 .. 32 runs the filter with 32-entry bound lists (no batched
