@@ -37,22 +37,24 @@ __device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) 
     float rk[E];
     int ri[E];
     __syncthreads();  // the caller's writes of key/idx are visible
-    if (active)
+    if (active) {
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             rk[j] = key[t * E + j];
             ri[j] = idx[t * E + j];
         }
+    }
     for (int size = 2; size <= N; size <<= 1) {
         int stride = size >> 1;
         if (stride >= W) {  // cross-warp strides (nthreads > 32 only)
             __syncthreads();  // everyone is done reading the previous shared phase
-            if (active)
+            if (active) {
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     key[t * E + j] = rk[j];
                     idx[t * E + j] = ri[j];
                 }
+            }
             for (; stride >= W; stride >>= 1) {
                 __syncthreads();
                 for (int i = t; i < (N >> 1); i += blockDim.x) {
@@ -70,12 +72,13 @@ __device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) 
                 }
             }
             __syncthreads();
-            if (active)
+            if (active) {
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     rk[j] = key[t * E + j];
                     ri[j] = idx[t * E + j];
                 }
+            }
         }
         if (!active) continue;
         for (; stride >= E; stride >>= 1) {  // partner in lane ^ (stride / E), same slot
@@ -112,12 +115,13 @@ __device__ void bitonic_sort_kv_regs(float* key, int* idx, int N, int nthreads) 
         }
     }
     __syncthreads();
-    if (active)
+    if (active) {
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             key[t * E + j] = rk[j];
             idx[t * E + j] = ri[j];
         }
+    }
     __syncthreads();
 }
 

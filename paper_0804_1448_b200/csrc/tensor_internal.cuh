@@ -339,18 +339,20 @@ struct RegList {
 #pragma unroll
         for (int i = 0; i < 16; ++i) ce(c[i], c[i + 16]);
 #pragma unroll
-        for (int st = 8; st > 0; st >>= 1)
+        for (int st = 8; st > 0; st >>= 1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
                 if ((i & st) == 0) ce(c[i], c[i + st]);
+        }
         if (KR > 16) {  // the 8 smallest of the upper half, sorted
 #pragma unroll
             for (int i = 0; i < 8; ++i) c[16 + i] = fminf(c[16 + i], c[24 + i]);
 #pragma unroll
-            for (int st = 4; st > 0; st >>= 1)
+            for (int st = 4; st > 0; st >>= 1) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                     if ((i & st) == 0) ce(c[16 + i], c[16 + i + st]);
+            }
         }
 #pragma unroll
         for (int s = 0; s < KR; ++s) key[s] = c[s];
