@@ -413,13 +413,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         float v_[32];                                                                            \
         _Pragma("unroll") for (int j_ = 0; j_ < 32; ++j_) v_[j_] = __uint_as_float(rr[j_]);      \
         if (!FOLD) add_rnorm_smem(v_, rnw + ((colb) - col_base));                                \
-        float m_[11];                                                                            \
-        _Pragma("unroll") for (int i_ = 0; i_ < 10; ++i_)                                        \
-            m_[i_] = min3(v_[3 * i_], v_[3 * i_ + 1], v_[3 * i_ + 2]);                           \
-        m_[10] = fminf(v_[30], v_[31]);                                                          \
-        const float cm_ = min3(min3(m_[0], m_[1], m_[2]), min3(m_[3], m_[4], m_[5]),             \
-                               min3(min3(m_[6], m_[7], m_[8]), m_[9], m_[10]));                  \
-        if (__any_sync(0xffffffffu, cm_ <= tlog)) {                                              \
+        /* log_all: nearly every chunk has a loggable value for some query of */               \
+        /* the warp (dense logs), so the minimum tree and vote are skipped */                   \
+        bool go_ = a.log_all != 0;                                                               \
+        if (!go_) {                                                                              \
+            float m_[11];                                                                        \
+            _Pragma("unroll") for (int i_ = 0; i_ < 10; ++i_)                                    \
+                m_[i_] = min3(v_[3 * i_], v_[3 * i_ + 1], v_[3 * i_ + 2]);                       \
+            m_[10] = fminf(v_[30], v_[31]);                                                      \
+            const float cm_ = min3(min3(m_[0], m_[1], m_[2]), min3(m_[3], m_[4], m_[5]),         \
+                                   min3(min3(m_[6], m_[7], m_[8]), m_[9], m_[10]));              \
+            go_ = __any_sync(0xffffffffu, cm_ <= tlog);                                          \
+        }                                                                                        \
+        if (go_) {                                                                               \
             float2* const v0_ = vlp;                                                             \
             _Pragma("unroll") for (int e_ = 0; e_ < 32; ++e_)                                    \
                 asm volatile(                                                                    \

@@ -128,6 +128,7 @@ struct FilterArgs {
     int W;
     int seed_off;          // 0 / 1: interleaved seed tile positions (retry uses fresh tiles)
     int seed_rank;         // T0 = thresh(seed_rank-th smallest seed group minimum)
+    int log_all;           // fixed filter: append without the per-chunk vote (dense logs)
     float* t0;             // [n_pad]
     float2* vlog;          // [parts][128][CV]
     int CV;

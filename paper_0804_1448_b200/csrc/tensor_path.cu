@@ -281,6 +281,13 @@ void tensor_search(DeviceContext& ctx, cudaStream_t stream, const TensorRefs& re
         // seed: W tiles whose 32nd smallest group minimum estimates the
         // (margin*k)-th smallest A (rank ~ m * 32 / (128 W)), W >= 2
         fa.seed_rank = 32;
+        // a warp's 32 queries x 32 columns hold ~1024 x (margin k) / m loggable
+        // values: from ~6 on some query hits practically every chunk and the
+        // vote only costs (config D: k = 100 / 256 filter 883 -> 859 / 793 ->
+        // 775 us; at k = 33, ~2.6 expected, skipping it measured slower;
+        // dev knob KNN_B200_LOG_ALL=0/1 overrides)
+        fa.log_all = 1024.0 * margin * k / static_cast<double>(m) >= 6.0 ? 1 : 0;
+        if (const char* e = std::getenv("KNN_B200_LOG_ALL")) fa.log_all = std::atoi(e) != 0;
         fa.W = static_cast<int>(std::min<int64_t>(
             rtiles, std::max<int64_t>(2, (m + 4LL * margin * k - 1) / (4LL * margin * k))));
         fa.seed_off = 0;
