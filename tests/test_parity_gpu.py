@@ -550,6 +550,39 @@ def test_non_finite_detected_on_device(knn, oracle):
     assert compare(t.index[:50], t.distance[:50], ri, rd, Q[:50], R, oracle=oracle).ok
 
 
+@pytest.mark.gpu
+def test_non_finite_detected_device_api(knn, oracle):
+    """The synchronous device-pointer API checks the caller's values first
+    (PointSet semantics) with the 16-byte-load scan: the first offending
+    coordinate is reported in the aligned middle, in the scalar head of a
+    misaligned pointer and in the scalar tail."""
+    import torch
+    n, m, d, k = 300, 2000, 13, 5  # n*d, m*d not multiples of 4: scalar tails
+    R = torch.from_numpy(oracle.uniform_f32(m, d, 43)).cuda()
+    flat = torch.from_numpy(oracle.uniform_f32(n * d + 1, 1, 44).ravel()).cuda()
+    Q = flat[1:].view(n, d)  # 4 bytes past a 16-byte boundary: scalar head
+    od = torch.empty((n, k), device="cuda")
+    oi = torch.empty((n, k), dtype=torch.int64, device="cuda")
+    go = lambda q, r: knn.search_device(q.data_ptr(), n, r.data_ptr(), m, d, k, od.data_ptr(), oi.data_ptr())
+    go(Q, R)
+    torch.cuda.synchronize()
+    for (qi, qc) in [(0, 1), (100, 7), (n - 1, d - 1)]:
+        Qb = Q.clone() if (qi, qc) != (0, 1) else Q
+        saved = Qb[qi, qc].item()
+        Qb[qi, qc] = float("nan")
+        with pytest.raises(ValueError, match=rf"^PointSet: non-finite coordinate at point {qi}, dimension {qc}$"):
+            go(Qb, R)
+        Qb[qi, qc] = saved
+    Rb = R.clone()
+    Rb[m - 1, d - 1] = float("inf")
+    with pytest.raises(ValueError, match=rf"^PointSet: non-finite coordinate at point {m - 1}, dimension {d - 1}$"):
+        go(Q, Rb)
+    go(Q, R)
+    torch.cuda.synchronize()
+    ri, _ = oracle.knn(Q[:20].cpu().numpy(), R.cpu().numpy(), k)
+    assert (oi[:20].cpu().numpy() == ri).all()
+
+
 def test_pipelined_host_search(knn, oracle):
     """n >= 2 pipeline chunks: the one-shot host API overlaps query H2D / D2H
     with the search.  Results, device-side value checks and the deferred
