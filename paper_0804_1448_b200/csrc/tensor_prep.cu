@@ -225,8 +225,11 @@ __global__ void __launch_bounds__(256) convert_kernel(PrepArgs a) {
 // per-row sums reduce over the 4 lanes (2 shuffle levels instead of 5).  The
 // arithmetic per coordinate is convert_kernel's, so Xh, the norms and the
 // radii agree with it up to the (exact-double) summation order.
+#ifndef KNN_CONVERT_MINB
+#define KNN_CONVERT_MINB 5  // 5 resident blocks per SM (<= 48 registers): config B's 600 blocks in one wave
+#endif
 template <bool QUERY, int GPL>  // GPL: granules per lane (d <= 16 GPL)
-__global__ void __launch_bounds__(256) convert4_kernel(PrepArgs a) {
+__global__ void __launch_bounds__(256, KNN_CONVERT_MINB) convert4_kernel(PrepArgs a) {
     if (QUERY) sm100::pdl_trigger();
     __shared__ float red[2][8];
     const int lane = threadIdx.x & 31;
