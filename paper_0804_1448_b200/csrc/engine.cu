@@ -29,6 +29,22 @@ DeviceArena::~DeviceArena() {
 
 namespace {
 thread_local bool t_capturing = false;  // the bound stream is being captured into a graph
+
+// queries per tensor-path search of a device-pointer call (multiple of the
+// 256-query pair; dev knob KNN_B200_TENSOR_CHUNK)
+int64_t tensor_query_chunk() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("KNN_B200_TENSOR_CHUNK");
+        const int64_t c = e ? std::max<int64_t>(256, std::atoll(e)) : int64_t{1} << 18;
+        return (c + 255) / 256 * 256;
+    }();
+    return v;
+}
+
+// fb[1] = (first ? 0 : fb[1]) + fb[0]: the fallback count summed over query chunks
+__global__ void sum_count_kernel(int* fb, bool first) {
+    if (threadIdx.x == 0) fb[1] = (first ? 0 : fb[1]) + fb[0];
+}
 }
 
 void DeviceArena::reserve(size_t bytes) {
@@ -62,7 +78,7 @@ Scratch& DeviceContext::bind(cudaStream_t st) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     KNN_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
     t_capturing = cs != cudaStreamCaptureStatusNone;
-    if (!slot->fb_dev && !t_capturing) KNN_CUDA_CHECK(cudaMalloc(&slot->fb_dev, sizeof(int)));
+    if (!slot->fb_dev && !t_capturing) KNN_CUDA_CHECK(cudaMalloc(&slot->fb_dev, 2 * sizeof(int)));
     s = slot.get();
     last = s;
     return *s;
@@ -172,6 +188,31 @@ void search_device(DeviceContext& ctx, cudaStream_t stream, const float* dQ, int
                    int raw_keys, int64_t index_base, float* d_out, int64_t* d_idx,
                    const TensorRefs* refs) {
     const SearchPlan plan = plan_search(n, m, d, k, metric, path);
+    const int64_t qchunk = tensor_query_chunk();
+    if (plan.path == 2 && n > qchunk) {
+        // query chunks bound the per-search scratch (the group logs grow as
+        // n x parts x log capacity); the reference set is prepared once and
+        // the fallback count summed over the chunks on the device
+        TensorRefs local;
+        const TensorRefs* rp = refs;
+        if (!rp) {
+            ctx.s->refs.reserve(tensor_refs_bytes(m, d));
+            tensor_prep_refs(stream, dR, m, d, ctx.s->refs.base(), local);
+            rp = &local;
+        }
+        int* fb = ctx.s->fb_dev;
+        for (int64_t q0 = 0; q0 < n; q0 += qchunk) {
+            const int64_t nq = std::min(qchunk, n - q0);
+            tensor_search(ctx, stream, *rp, dQ + q0 * d, nq, k, raw_keys, index_base, d_out + q0 * k,
+                          d_idx + q0 * k);
+            if (fb) {
+                sum_count_kernel<<<1, 32, 0, stream>>>(fb, q0 == 0);
+                KNN_LAUNCH_CHECK();
+            }
+        }
+        if (fb) KNN_CUDA_CHECK(cudaMemcpyAsync(fb, fb + 1, sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        return;
+    }
     if (plan.path == 2) {
         if (refs)  // reference set already prepared (index handle)
             tensor_search(ctx, stream, *refs, dQ, n, k, raw_keys, index_base, d_out, d_idx);

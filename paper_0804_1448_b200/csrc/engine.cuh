@@ -40,6 +40,7 @@ struct Scratch {
     DeviceArena xl;          // exact large-k selection (also the tensor path's large-k fallback)
     int last_fallbacks = 0;  // tensor path: queries re-run on the exact kernel
     int* fb_dev = nullptr;   // ... the same count, when resolved on the device
+                             // ([0] the count, [1] a running sum over query chunks)
     bool fb_on_device = false;
     ~Scratch();
 };

@@ -583,6 +583,31 @@ def test_non_finite_detected_device_api(knn, oracle):
     assert (oi[:20].cpu().numpy() == ri).all()
 
 
+@pytest.mark.gpu
+def test_device_search_query_chunks(knn, oracle):
+    """A device-pointer search over more queries than one tensor-path chunk
+    (262144): rows on both sides of the chunk boundary are exact, and the
+    fallback count is summed over the chunks (tie-saturated queries in each)."""
+    import torch
+    n, m, d, k = 300000, 20000, 16, 10
+    R = oracle.uniform_f32(m, d, 45)
+    R[:200] = 5.0  # 200 copies of one point far from the rest
+    Q = oracle.uniform_f32(n, d, 46)
+    Q[1000:1100] = R[0]  # their 200 tied neighbours overflow the fast path
+    Q[280000:280100] = R[0]
+    Qd, Rd = torch.from_numpy(Q).cuda(), torch.from_numpy(R).cuda()
+    od = torch.empty((n, k), device="cuda")
+    oi = torch.empty((n, k), dtype=torch.int64, device="cuda")
+    knn.search_device(Qd.data_ptr(), n, Rd.data_ptr(), m, d, k, od.data_ptr(), oi.data_ptr(),
+                      path=knn.PATH_TENSOR)
+    torch.cuda.synchronize()
+    assert knn.last_fallback_count() == 200
+    rows = np.r_[0:64, 1000:1100:10, 262100:262200, 280000:280100:10, n - 64:n]
+    te = knn.bf_knn(Q[rows], R, k, config=knn.BfConfig(path=knn.PATH_EXACT))
+    assert (oi.cpu().numpy()[rows] == te.index).all()
+    assert (od.cpu().numpy()[rows] == te.distance).all()
+
+
 def test_pipelined_host_search(knn, oracle):
     """n >= 2 pipeline chunks: the one-shot host API overlaps query H2D / D2H
     with the search.  Results, device-side value checks and the deferred
